@@ -1,0 +1,179 @@
+/*
+ * hetccl.h — C ABI of the B200-native hierarchical collective library (HetCCL hot path,
+ * arXiv 2601.22585). Pure C; no torch or CUDA types in the signatures (a stream is passed as the
+ * opaque `hetcclStream_t`, which IS a `cudaStream_t`; pass 0 for the legacy default stream).
+ *
+ * What the library computes (see DESIGN.md §1-3 for the full readings):
+ *   All-Reduce, Reduce-Scatter, All-Gather and Broadcast over n ranks split into D "device
+ *   domains" (the paper's vendor groups). The paper evaluates exactly these collectives
+ *   (§5.2 "All-Reduce, All-Gather, Reduce-Scatter, Reduce, Broadcast, and
+ *   All-to-All"; App. E.1) and composes them from vendor-local collectives plus a
+ *   cross-vendor layer (§4 "Key Approach"; §4.2). The composition it
+ *   leaves open is read as SPEC.md:350 / SPEC.md:404: intra-domain reduce-scatter -> cross-domain
+ *   exchange of partials -> intra-domain all-gather. Signatures, in-place rules and enum VALUES copy
+ *   NCCL's, because the paper's boundary is "intercepting and overriding NCCL or RCCL symbols"
+ *   (§4.4).
+ *
+ * Floating-point order (reading R3): for every element, ascending rank within each
+ * domain, then ascending domain id; 16-bit types accumulate in fp32 and are rounded (RNE) once at
+ * the domain boundary and once at the end (reading R6). int32 sums wrap mod 2^32 (reading R8).
+ * Results are deterministic and identical on every rank.
+ *
+ * Ownership: the caller owns send/recv buffers and streams; buffers are device memory of the
+ * comm's device, must stay untouched until the stream passes the op, and need no registration.
+ * The library owns the comm, its scratch ring, flags and peer mappings until hetccl_comm_destroy.
+ *
+ * Ordering: every op is enqueued on `stream` and returns without a host sync. Every rank must issue
+ * the same ops in the same order with the same count/dtype/op/root (as in NCCL; a mismatch is
+ * undefined and not detected). One comm must not run two ops concurrently (use one comm per
+ * concurrent stream). A device-side spin timeout (HETCCL_TIMEOUT_S, default 30 s) ends a stuck
+ * op early; hetccl_comm_get_async_error then reports it.
+ *
+ * Errors are return codes only (no exceptions or abort across the ABI); the detail text of the
+ * last failure on a comm is available from hetccl_get_last_error.
+ */
+#ifndef HETCCL_H
+#define HETCCL_H
+
+#include <stddef.h>
+
+#if defined(__GNUC__)
+#define HETCCL_API __attribute__((visibility("default")))
+#else
+#define HETCCL_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HETCCL_VERSION 100 /* 0.1.0 */
+#define HETCCL_MAX_RANKS 16
+#define HETCCL_BLOB_BYTES 512 /* bytes per rank written by hetccl_comm_export */
+
+typedef struct hetcclComm* hetcclComm_t;
+struct CUstream_st;
+typedef struct CUstream_st* hetcclStream_t; /* == cudaStream_t */
+
+typedef enum {
+  hetcclSuccess = 0,
+  hetcclUnhandledCudaError = 1, /* a CUDA runtime call failed */
+  hetcclSystemError = 2,        /* IPC import / host allocation failed */
+  hetcclInternalError = 3,      /* device-side timeout or protocol failure */
+  hetcclInvalidArgument = 4,    /* null pointer, bad map/dtype/op/root/count, illegal overlap */
+  hetcclInvalidUsage = 5        /* comm not connected, wrong device, wrong comm kind */
+} hetcclResult_t;
+
+typedef enum { hetcclInt32 = 2, hetcclFloat16 = 6, hetcclFloat32 = 7, hetcclBfloat16 = 9 } hetcclDataType_t;
+typedef enum { hetcclSum = 0, hetcclMax = 2, hetcclMin = 3 } hetcclRedOp_t;
+
+/* ---------------------------------------------------------------- communicators ------------- */
+
+/* Library version (HETCCL_VERSION). */
+HETCCL_API hetcclResult_t hetccl_get_version(int* version);
+
+/*
+ * Map validation only (no CUDA): rank_to_domain[r] in [0, D) for r in [0, nranks), ids dense
+ * (every id 0..D-1 used), 1 <= nranks <= HETCCL_MAX_RANKS. Writes D to *ndomains if non-null.
+ * Returns hetcclInvalidArgument otherwise.
+ */
+HETCCL_API hetcclResult_t hetccl_validate_map(int nranks, const int* rank_to_domain, int* ndomains);
+
+/*
+ * One process per GPU, two-phase bootstrap:
+ *   hetccl_comm_init   allocates this rank's symmetric scratch ring + flags on `cuda_device`
+ *                      (the map is copied; identical on all ranks);
+ *   hetccl_comm_export writes this rank's HETCCL_BLOB_BYTES-byte blob (CUDA IPC handles) to `blob`
+ *                      (*blob_bytes in: capacity, out: bytes written);
+ *   the caller all-gathers the blobs (e.g. torch.distributed.all_gather_object over gloo), then
+ *   hetccl_comm_connect takes nranks blobs concatenated in rank order (blob_bytes = nranks *
+ *                      HETCCL_BLOB_BYTES), opens the peers' memory and checks that every rank
+ *                      passed the same map and geometry (hetcclInvalidUsage if not).
+ */
+HETCCL_API hetcclResult_t hetccl_comm_init(hetcclComm_t* comm, int nranks, int rank, const int* rank_to_domain,
+                                int cuda_device);
+HETCCL_API hetcclResult_t hetccl_comm_export(hetcclComm_t comm, void* blob, size_t* blob_bytes);
+HETCCL_API hetcclResult_t hetccl_comm_connect(hetcclComm_t comm, const void* blobs, size_t blob_bytes);
+
+/* Single process driving ndev GPUs (tests, bench): comms[i] is rank i on device devlist[i];
+ * peer access is enabled between all pairs. Ops are then issued per comm (any order of launch). */
+HETCCL_API hetcclResult_t hetccl_comm_init_all(hetcclComm_t* comms, int ndev, const int* devlist, const int* rank_to_domain);
+
+/*
+ * Rank-multiplexed comm: all `nranks` logical ranks live on ONE device and every op runs as ONE
+ * cooperative kernel over all ranks' buffers (rank = blockIdx.y). Same device code and protocol as
+ * the multi-GPU path; used to check 8-rank splits on fewer GPUs and for the 1-GPU
+ * bench. Use the hetccl_mux_* entry points with per-rank buffer arrays.
+ */
+HETCCL_API hetcclResult_t hetccl_comm_init_mux(hetcclComm_t* comm, int nranks, const int* rank_to_domain, int cuda_device);
+
+/* Frees scratch, flags and peer mappings. Synchronizes the comm's device first. */
+HETCCL_API hetcclResult_t hetccl_comm_destroy(hetcclComm_t comm);
+
+/* Rank, size, domain of this rank, number of domains, index within its domain, domain size. */
+HETCCL_API hetcclResult_t hetccl_comm_info(hetcclComm_t comm, int* rank, int* nranks, int* domain, int* ndomains,
+                                int* domain_rank, int* domain_size);
+
+/* hetcclInternalError if a device-side timeout was recorded on this comm since init (sticky). */
+HETCCL_API hetcclResult_t hetccl_comm_get_async_error(hetcclComm_t comm);
+
+HETCCL_API const char* hetccl_get_error_string(hetcclResult_t r);
+HETCCL_API const char* hetccl_get_last_error(hetcclComm_t comm); /* detail of the last non-success on comm */
+
+/* ----------------------------------------------------------------- collectives ------------- */
+/*
+ * All pointers are device pointers on the comm's device. count == 0 is a successful no-op.
+ *
+ * hetccl_allreduce: recvbuf[i] = reduction over all ranks of sendbuf[i], i < count; identical on
+ *   every rank. In place iff sendbuf == recvbuf.
+ * hetccl_reduce_scatter: sendbuf holds nranks*recvcount elements; rank r receives block r of the
+ *   reduction. In place iff recvbuf == sendbuf + rank*recvcount (elements).
+ * hetccl_all_gather: recvbuf holds nranks*sendcount elements; block j is rank j's sendbuf.
+ *   In place iff sendbuf == recvbuf + rank*sendcount.
+ * hetccl_broadcast: every rank's recvbuf = root's sendbuf (count elements); sendbuf is read on the
+ *   root only (may be NULL elsewhere). In place iff sendbuf == recvbuf.
+ * Any other overlap of send and recv ranges is hetcclInvalidArgument.
+ */
+HETCCL_API hetcclResult_t hetccl_allreduce(const void* sendbuf, void* recvbuf, size_t count, hetcclDataType_t dt,
+                                hetcclRedOp_t op, hetcclComm_t comm, hetcclStream_t stream);
+HETCCL_API hetcclResult_t hetccl_reduce_scatter(const void* sendbuf, void* recvbuf, size_t recvcount, hetcclDataType_t dt,
+                                     hetcclRedOp_t op, hetcclComm_t comm, hetcclStream_t stream);
+HETCCL_API hetcclResult_t hetccl_all_gather(const void* sendbuf, void* recvbuf, size_t sendcount, hetcclDataType_t dt,
+                                 hetcclComm_t comm, hetcclStream_t stream);
+HETCCL_API hetcclResult_t hetccl_broadcast(const void* sendbuf, void* recvbuf, size_t count, hetcclDataType_t dt, int root,
+                                hetcclComm_t comm, hetcclStream_t stream);
+
+/* Rank-multiplexed variants: sendbufs[r] / recvbufs[r] for every logical rank r of a mux comm. */
+HETCCL_API hetcclResult_t hetccl_mux_allreduce(const void* const* sendbufs, void* const* recvbufs, size_t count,
+                                    hetcclDataType_t dt, hetcclRedOp_t op, hetcclComm_t comm, hetcclStream_t stream);
+HETCCL_API hetcclResult_t hetccl_mux_reduce_scatter(const void* const* sendbufs, void* const* recvbufs, size_t recvcount,
+                                         hetcclDataType_t dt, hetcclRedOp_t op, hetcclComm_t comm,
+                                         hetcclStream_t stream);
+HETCCL_API hetcclResult_t hetccl_mux_all_gather(const void* const* sendbufs, void* const* recvbufs, size_t sendcount,
+                                     hetcclDataType_t dt, hetcclComm_t comm, hetcclStream_t stream);
+HETCCL_API hetcclResult_t hetccl_mux_broadcast(const void* const* sendbufs, void* const* recvbufs, size_t count,
+                                    hetcclDataType_t dt, int root, hetcclComm_t comm, hetcclStream_t stream);
+
+/* ------------------------------------------------------------- plan introspection ----------- */
+/*
+ * Host-only (no CUDA): the per-rank algorithmic NVLink bytes one op moves, from the same plan the
+ * kernels execute. op: 0 allreduce, 1 reduce_scatter, 2 all_gather, 3 broadcast.
+ * count = the op's `count` argument (recvcount / sendcount for RS / AG). Writes bytes sent and
+ * received by `rank` over the peer fabric, and the tile geometry (elements per tile, tiles,
+ * channels) the launch would use with `nchannels` channels (0 = default).
+ */
+typedef struct {
+  size_t bytes_sent;
+  size_t bytes_recv;
+  size_t tile_elems;
+  size_t ntiles;
+  int nchannels;
+  int nslots;
+} hetcclPlanInfo_t;
+HETCCL_API hetcclResult_t hetccl_plan_info(int nranks, const int* rank_to_domain, int rank, int op, size_t count,
+                                hetcclDataType_t dt, int root, int nchannels, hetcclPlanInfo_t* info);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HETCCL_H */

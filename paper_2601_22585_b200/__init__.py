@@ -1,0 +1,274 @@
+"""Python binding of libhetccl.so (include/hetccl.h) — argument marshalling only.
+
+Every collective runs in the library's sm_100a kernels; this module converts torch tensors / ints
+to pointers and sizes, raises on a non-success return code, and offers a torch.distributed
+bootstrap for the one-process-per-GPU mode (the blob exchange of SURVEY §3.2). There is no CPU
+fallback: importing a collective without the built extension raises.
+
+Function names follow the C ABI (``hetccl_allreduce`` ...); ``allreduce`` etc. are the same calls
+taking tensors.
+"""
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libhetccl.so")
+
+INT32, FLOAT16, FLOAT32, BFLOAT16 = 2, 6, 7, 9
+SUM, MAX, MIN = 0, 2, 3
+OP_ALLREDUCE, OP_REDUCE_SCATTER, OP_ALL_GATHER, OP_BROADCAST = 0, 1, 2, 3
+BLOB_BYTES = 512
+MAX_RANKS = 16
+_RESULT = {0: "hetcclSuccess", 1: "hetcclUnhandledCudaError", 2: "hetcclSystemError", 3: "hetcclInternalError",
+           4: "hetcclInvalidArgument", 5: "hetcclInvalidUsage"}
+_OPS = {"sum": SUM, "max": MAX, "min": MIN}
+
+
+class HetcclError(RuntimeError):
+    def __init__(self, code, detail=""):
+        self.code = code
+        super().__init__(f"{_RESULT.get(code, code)}: {detail}")
+
+
+class PlanInfo(ctypes.Structure):
+    _fields_ = [("bytes_sent", ctypes.c_size_t), ("bytes_recv", ctypes.c_size_t), ("tile_elems", ctypes.c_size_t),
+                ("ntiles", ctypes.c_size_t), ("nchannels", ctypes.c_int), ("nslots", ctypes.c_int)]
+
+
+EXPORTED = [
+    "hetccl_get_version", "hetccl_validate_map", "hetccl_comm_init", "hetccl_comm_export", "hetccl_comm_connect",
+    "hetccl_comm_init_all", "hetccl_comm_init_mux", "hetccl_comm_destroy", "hetccl_comm_info",
+    "hetccl_comm_get_async_error", "hetccl_get_error_string", "hetccl_get_last_error", "hetccl_allreduce",
+    "hetccl_reduce_scatter", "hetccl_all_gather", "hetccl_broadcast", "hetccl_mux_allreduce",
+    "hetccl_mux_reduce_scatter", "hetccl_mux_all_gather", "hetccl_mux_broadcast", "hetccl_plan_info",
+]
+
+_lib = None
+
+
+def lib():
+    """Load libhetccl.so (built in-tree by build.py / __graft_entry__.build()). Raises if missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_LIB_PATH):
+        raise ImportError(f"{_LIB_PATH} is missing: build it with `python -m paper_2601_22585_b200.build`")
+    L = ctypes.CDLL(_LIB_PATH)
+    c_int, c_size, vp, pp = ctypes.c_int, ctypes.c_size_t, ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p)
+    ip = ctypes.POINTER(ctypes.c_int)
+    sig = {
+        "hetccl_get_version": [ip],
+        "hetccl_validate_map": [c_int, ip, ip],
+        "hetccl_comm_init": [pp, c_int, c_int, ip, c_int],
+        "hetccl_comm_export": [vp, vp, ctypes.POINTER(c_size)],
+        "hetccl_comm_connect": [vp, vp, c_size],
+        "hetccl_comm_init_all": [pp, c_int, ip, ip],
+        "hetccl_comm_init_mux": [pp, c_int, ip, c_int],
+        "hetccl_comm_destroy": [vp],
+        "hetccl_comm_info": [vp, ip, ip, ip, ip, ip, ip],
+        "hetccl_comm_get_async_error": [vp],
+        "hetccl_allreduce": [vp, vp, c_size, c_int, c_int, vp, vp],
+        "hetccl_reduce_scatter": [vp, vp, c_size, c_int, c_int, vp, vp],
+        "hetccl_all_gather": [vp, vp, c_size, c_int, vp, vp],
+        "hetccl_broadcast": [vp, vp, c_size, c_int, c_int, vp, vp],
+        "hetccl_mux_allreduce": [pp, pp, c_size, c_int, c_int, vp, vp],
+        "hetccl_mux_reduce_scatter": [pp, pp, c_size, c_int, c_int, vp, vp],
+        "hetccl_mux_all_gather": [pp, pp, c_size, c_int, vp, vp],
+        "hetccl_mux_broadcast": [pp, pp, c_size, c_int, c_int, vp, vp],
+        "hetccl_plan_info": [c_int, ip, c_int, c_int, c_size, c_int, c_int, c_int, ctypes.POINTER(PlanInfo)],
+    }
+    for name, args in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = c_int
+    L.hetccl_get_error_string.argtypes = [c_int]
+    L.hetccl_get_error_string.restype = ctypes.c_char_p
+    L.hetccl_get_last_error.argtypes = [vp]
+    L.hetccl_get_last_error.restype = ctypes.c_char_p
+    _lib = L
+    return L
+
+
+def _check(rc, comm=None):
+    if rc != 0:
+        detail = ""
+        if comm is not None:
+            detail = (lib().hetccl_get_last_error(comm) or b"").decode()
+        raise HetcclError(rc, detail or lib().hetccl_get_error_string(rc).decode())
+
+
+def _imap(seq):
+    return (ctypes.c_int * len(seq))(*[int(v) for v in seq])
+
+
+# ------------------------------------------------------------------------------ dtype mapping
+def dtype_code(dt):
+    import torch
+    m = {torch.int32: INT32, torch.float16: FLOAT16, torch.float32: FLOAT32, torch.bfloat16: BFLOAT16}
+    if dt not in m:
+        raise HetcclError(4, f"unsupported dtype {dt}")
+    return m[dt]
+
+
+def _op(op):
+    return _OPS[op] if isinstance(op, str) else int(op)
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def _ptr(t):
+    return None if t is None else (t if isinstance(t, int) else t.data_ptr())
+
+
+# ------------------------------------------------------------------------------ communicators
+def hetccl_validate_map(rank_to_domain):
+    nd = ctypes.c_int(0)
+    _check(lib().hetccl_validate_map(len(rank_to_domain), _imap(rank_to_domain), ctypes.byref(nd)))
+    return nd.value
+
+
+def hetccl_comm_init(nranks, rank, rank_to_domain, device):
+    c = ctypes.c_void_p()
+    _check(lib().hetccl_comm_init(ctypes.byref(c), nranks, rank, _imap(rank_to_domain), device))
+    return c
+
+
+def hetccl_comm_export(comm):
+    buf = ctypes.create_string_buffer(BLOB_BYTES)
+    n = ctypes.c_size_t(BLOB_BYTES)
+    _check(lib().hetccl_comm_export(comm, buf, ctypes.byref(n)), comm)
+    return buf.raw[: n.value]
+
+
+def hetccl_comm_connect(comm, blobs):
+    data = b"".join(blobs) if isinstance(blobs, (list, tuple)) else blobs
+    _check(lib().hetccl_comm_connect(comm, data, len(data)), comm)
+
+
+def hetccl_comm_init_all(devlist, rank_to_domain):
+    n = len(devlist)
+    arr = (ctypes.c_void_p * n)()
+    _check(lib().hetccl_comm_init_all(arr, n, _imap(devlist), _imap(rank_to_domain)))
+    return [ctypes.c_void_p(arr[i]) for i in range(n)]
+
+
+def hetccl_comm_init_mux(nranks, rank_to_domain, device):
+    c = ctypes.c_void_p()
+    _check(lib().hetccl_comm_init_mux(ctypes.byref(c), nranks, _imap(rank_to_domain), device))
+    return c
+
+
+def hetccl_comm_destroy(comm):
+    _check(lib().hetccl_comm_destroy(comm))
+
+
+def hetccl_comm_info(comm):
+    v = [ctypes.c_int(0) for _ in range(6)]
+    _check(lib().hetccl_comm_info(comm, *[ctypes.byref(x) for x in v]), comm)
+    keys = ("rank", "nranks", "domain", "ndomains", "domain_rank", "domain_size")
+    return dict(zip(keys, [x.value for x in v]))
+
+
+def hetccl_comm_get_async_error(comm):
+    _check(lib().hetccl_comm_get_async_error(comm), comm)
+
+
+def hetccl_plan_info(rank_to_domain, rank, op, count, dtype=BFLOAT16, root=0, nchannels=0):
+    info = PlanInfo()
+    _check(lib().hetccl_plan_info(len(rank_to_domain), _imap(rank_to_domain), rank, op, count, dtype, root,
+                                  nchannels, ctypes.byref(info)))
+    return {f: getattr(info, f) for f, _ in PlanInfo._fields_}
+
+
+def init_process_group_comm(rank_to_domain, rank=None, world_size=None, device=None, group=None):
+    """One process per GPU: init this rank's comm, all-gather the IPC blobs over torch.distributed
+    (object collective on `group`), connect. Returns the comm handle."""
+    import torch
+    import torch.distributed as dist
+    rank = dist.get_rank(group) if rank is None else rank
+    world_size = dist.get_world_size(group) if world_size is None else world_size
+    device = torch.cuda.current_device() if device is None else device
+    comm = hetccl_comm_init(world_size, rank, rank_to_domain, device)
+    blob = hetccl_comm_export(comm)
+    blobs = [None] * world_size
+    dist.all_gather_object(blobs, blob, group=group)
+    hetccl_comm_connect(comm, blobs)
+    return comm
+
+
+# ------------------------------------------------------------------------------ collectives
+def hetccl_allreduce(sendbuf, recvbuf, count, dtype, op, comm, stream):
+    _check(lib().hetccl_allreduce(sendbuf, recvbuf, count, dtype, _op(op), comm, stream), comm)
+
+
+def hetccl_reduce_scatter(sendbuf, recvbuf, recvcount, dtype, op, comm, stream):
+    _check(lib().hetccl_reduce_scatter(sendbuf, recvbuf, recvcount, dtype, _op(op), comm, stream), comm)
+
+
+def hetccl_all_gather(sendbuf, recvbuf, sendcount, dtype, comm, stream):
+    _check(lib().hetccl_all_gather(sendbuf, recvbuf, sendcount, dtype, comm, stream), comm)
+
+
+def hetccl_broadcast(sendbuf, recvbuf, count, dtype, root, comm, stream):
+    _check(lib().hetccl_broadcast(sendbuf, recvbuf, count, dtype, root, comm, stream), comm)
+
+
+def _parr(xs):
+    return (ctypes.c_void_p * len(xs))(*[_ptr(x) for x in xs])
+
+
+def hetccl_mux_allreduce(sendbufs, recvbufs, count, dtype, op, comm, stream):
+    _check(lib().hetccl_mux_allreduce(_parr(sendbufs), _parr(recvbufs), count, dtype, _op(op), comm, stream), comm)
+
+
+def hetccl_mux_reduce_scatter(sendbufs, recvbufs, recvcount, dtype, op, comm, stream):
+    _check(lib().hetccl_mux_reduce_scatter(_parr(sendbufs), _parr(recvbufs), recvcount, dtype, _op(op), comm, stream),
+           comm)
+
+
+def hetccl_mux_all_gather(sendbufs, recvbufs, sendcount, dtype, comm, stream):
+    _check(lib().hetccl_mux_all_gather(_parr(sendbufs), _parr(recvbufs), sendcount, dtype, comm, stream), comm)
+
+
+def hetccl_mux_broadcast(sendbufs, recvbufs, count, dtype, root, comm, stream):
+    _check(lib().hetccl_mux_broadcast(_parr(sendbufs), _parr(recvbufs), count, dtype, root, comm, stream), comm)
+
+
+# tensor conveniences (same calls; count/dtype taken from the tensors)
+def allreduce(send, recv, comm, op="sum", stream=None):
+    hetccl_allreduce(_ptr(send), _ptr(recv), recv.numel(), dtype_code(recv.dtype), op, comm, _stream(stream))
+
+
+def reduce_scatter(send, recv, comm, op="sum", stream=None):
+    hetccl_reduce_scatter(_ptr(send), _ptr(recv), recv.numel(), dtype_code(recv.dtype), op, comm, _stream(stream))
+
+
+def all_gather(send, recv, comm, stream=None):
+    hetccl_all_gather(_ptr(send), _ptr(recv), send.numel(), dtype_code(send.dtype), comm, _stream(stream))
+
+
+def broadcast(send, recv, root, comm, stream=None):
+    hetccl_broadcast(_ptr(send), _ptr(recv), recv.numel(), dtype_code(recv.dtype), root, comm, _stream(stream))
+
+
+def mux_allreduce(sends, recvs, comm, op="sum", stream=None):
+    hetccl_mux_allreduce(sends, recvs, recvs[0].numel(), dtype_code(recvs[0].dtype), op, comm, _stream(stream))
+
+
+def mux_reduce_scatter(sends, recvs, comm, op="sum", stream=None):
+    hetccl_mux_reduce_scatter(sends, recvs, recvs[0].numel(), dtype_code(recvs[0].dtype), op, comm, _stream(stream))
+
+
+def mux_all_gather(sends, recvs, comm, stream=None):
+    hetccl_mux_all_gather(sends, recvs, sends[0].numel(), dtype_code(sends[0].dtype), comm, _stream(stream))
+
+
+def mux_broadcast(sends, recvs, root, comm, stream=None):
+    hetccl_mux_broadcast(sends, recvs, recvs[0].numel(), dtype_code(recvs[0].dtype), root, comm, _stream(stream))

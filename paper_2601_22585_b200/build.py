@@ -1,0 +1,48 @@
+"""Build libhetccl.so in-tree with nvcc for sm_100a (no JIT, no torch extension machinery).
+
+The library is the C ABI of include/hetccl.h; the Python binding (``__init__.py``) loads it with
+ctypes. Compiled with -lineinfo (ncu source view) and WITHOUT --use_fast_math (IEEE arithmetic,
+no flush-to-zero: DESIGN.md reading R9).
+"""
+import os
+import subprocess
+import sys
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+CSRC = os.path.join(HERE, "csrc")
+LIB = os.path.join(HERE, "libhetccl.so")
+SOURCES = ["kernels.cu", "runtime.cu", "plan.cpp"]
+HEADERS = ["hetccl_internal.h", os.path.join("..", "..", "include", "hetccl.h")]
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
+         "-Xcompiler", "-fPIC,-O2,-fvisibility=hidden", "-Xptxas", "-v", "--shared", "-cudart", "static"]
+
+
+def stale():
+    if not os.path.exists(LIB):
+        return True
+    t = os.path.getmtime(LIB)
+    files = [os.path.join(CSRC, f) for f in SOURCES + HEADERS] + [__file__]
+    return any(os.path.getmtime(f) > t for f in files)
+
+
+def build(force=False, verbose=False):
+    if not force and not stale():
+        return LIB
+    tmp = LIB + f".tmp{os.getpid()}"
+    cmd = [NVCC, *FLAGS, "-o", tmp] + [os.path.join(CSRC, s) for s in SOURCES]
+    p = subprocess.run(cmd, capture_output=True, text=True)
+    if p.returncode != 0:
+        sys.stderr.write(p.stdout + p.stderr)
+        raise RuntimeError("nvcc failed building libhetccl.so")
+    with open(os.path.join(HERE, "ptxas_info.txt"), "w") as f:
+        f.write(p.stderr)
+    if verbose:
+        sys.stderr.write(p.stderr)
+    os.replace(tmp, LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose=True)
+    print(LIB)

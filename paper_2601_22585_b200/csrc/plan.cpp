@@ -1,0 +1,269 @@
+// plan.cpp — host-side plan: domain topology, tile geometry, per-rank protocol constants and the
+// algorithmic per-rank byte counts. Pure C++, no CUDA; the kernels in
+// kernels.cu execute exactly this partition (the boundary formulas are restated there on the device).
+//
+// Partition of one AR tile of `len` elements:
+//   L = lcm(d_0..d_{D-1}) elementary segments, boundary b(s) = floor_V(len*s/L), b(L) = len
+//   (floor_V rounds down to a multiple of the 16-byte vector width V), so member j of domain k
+//   (size d) owns segments [j*L/d, (j+1)*L/d) and every segment has exactly one owner per domain
+//   (SURVEY §8(a) a0). Piece p of segment s (reduced by domain p's owner in the cross stage):
+//   c(s,p) = b(s) + floor_V((b(s+1)-b(s))*p/D), c(s,D) = b(s+1).
+#include <algorithm>
+#include <cstring>
+
+#include "hetccl_internal.h"
+
+namespace hetccl {
+
+static int gcd_(int a, int b) { return b ? gcd_(b, a % b) : a; }
+
+int build_topo(int n, const int* map, Topo* t) {
+  if (n < 1 || n > kMaxRanks || !map) return -1;
+  std::memset(t, 0, sizeof(*t));
+  int D = 0;
+  for (int r = 0; r < n; r++) {
+    if (map[r] < 0 || map[r] >= n) return -1;
+    D = std::max(D, map[r] + 1);
+  }
+  int pos = 0;
+  for (int k = 0; k < D; k++) {
+    t->dom_first[k] = pos;
+    for (int r = 0; r < n; r++)
+      if (map[r] == k) {
+        t->rank_dom[r] = k;
+        t->rank_idx[r] = pos - t->dom_first[k];
+        t->members[pos++] = r;
+      }
+    t->dom_size[k] = pos - t->dom_first[k];
+    if (t->dom_size[k] == 0) return -1;  // ids must be dense (reading R4)
+  }
+  int L = 1, dmin = n;
+  for (int k = 0; k < D; k++) {
+    L = L / gcd_(L, t->dom_size[k]) * t->dom_size[k];
+    dmin = std::min(dmin, t->dom_size[k]);
+  }
+  t->n = n;
+  t->D = D;
+  t->L = L;
+  t->dmin = dmin;
+  return 0;
+}
+
+static size_t floor_to(size_t x, size_t q) { return x / q * q; }
+static size_t ceil_div(size_t a, size_t b) { return (a + b - 1) / b; }
+
+// quantum (elements) a full tile must be a multiple of, so every boundary is V-aligned
+static size_t quantum(const Topo& t, int op, int V) {
+  if (op == OP_ALLREDUCE) return (size_t)t.L * t.D * V;
+  return (size_t)t.L * V;
+}
+
+size_t slot_mult_num(const Topo& t, int op, size_t tile) {
+  size_t dmin = (size_t)t.dmin, n = (size_t)t.n, D = (size_t)t.D;
+  switch (op) {
+    case OP_ALLREDUCE:  // s1[d][T/d] + s2[D][T/d] + ag[T/d] + s3[d][T/d]
+      return 2 * tile + (D + 1) * (tile / dmin);
+    case OP_REDUCE_SCATTER:  // s1[d][T + (n-d)T/d] + s2[D][T]
+      return n * tile + D * tile;
+    case OP_ALL_GATHER:  // s_in[d][T + (n-d)T/d] + xin[(n-d)T/d]
+      return n * tile + (n - dmin) * (tile / dmin);
+    case OP_BROADCAST:  // reg[T/d] + s3[d][T/d]
+      return tile + tile / dmin;
+    default:
+      return 0;
+  }
+}
+
+static size_t default_tile_bytes(int op, int n) {
+  const char* e = getenv("HETCCL_TILE_KB");
+  size_t b = e ? (size_t)atol(e) * 1024 : (size_t)512 * 1024;
+  if (op == OP_REDUCE_SCATTER || op == OP_ALL_GATHER) b /= (size_t)n;  // RS/AG tiles are per shard
+  return std::max<size_t>(b, 4096);
+}
+
+Geometry make_geometry(const Topo& t, int op, size_t count, int es, int nch_max, size_t slot_elems) {
+  Geometry g{0, 0, 0};
+  if (count == 0) return g;
+  const int V = 16 / es;
+  const size_t q = quantum(t, op, V);
+  // largest tile that fits a slot
+  size_t cap = q;
+  {
+    size_t lo = q, hi = std::max(q, slot_elems);
+    hi = floor_to(hi, q);
+    while (lo < hi) {  // binary search on multiples of q
+      size_t mid = floor_to(lo + (hi - lo) / 2 + q, q);
+      if (mid > hi) mid = hi;
+      if (slot_mult_num(t, op, mid) <= slot_elems) {
+        cap = mid;
+        if (mid == lo) break;
+        lo = mid;
+      } else {
+        hi = mid - q;
+      }
+    }
+    if (slot_mult_num(t, op, lo) <= slot_elems) cap = std::max(cap, lo);
+  }
+  size_t target = std::max(q, floor_to(default_tile_bytes(op, t.n) / es, q));
+  size_t tile = std::min(cap, target);
+  size_t per_ch = ceil_div(count, (size_t)nch_max);
+  if (per_ch < tile) tile = std::max(q, ceil_div(per_ch, q) * q);
+  g.tile = tile;
+  g.ntiles = ceil_div(count, tile);
+  g.nch = (int)std::min<size_t>((size_t)nch_max, g.ntiles);
+  return g;
+}
+
+static int owner_of(const Topo& t, int q, int s) {  // domain q's owner of elementary segment s
+  int dq = t.dom_size[q];
+  return t.members[t.dom_first[q] + s / (t.L / dq)];
+}
+
+void make_rank_plan(const Topo& t, int op, int rank, int root, RankPlan* rp) {
+  std::memset(rp, 0, sizeof(*rp));
+  const int k = t.rank_dom[rank], j = t.rank_idx[rank], d = t.dom_size[k], D = t.D, L = t.L, n = t.n;
+  uint32_t peers = 0;
+  for (int i = 0; i < d; i++)
+    if (i != j) peers |= 1u << t.members[t.dom_first[k] + i];
+  const int spj = L / d;
+  switch (op) {
+    case OP_ALLREDUCE: {
+      uint32_t cross = 0;
+      for (int s = j * spj; s < (j + 1) * spj; s++)
+        for (int q = 0; q < D; q++)
+          if (q != k) cross |= 1u << owner_of(t, q, s);
+      rp->partners = peers | cross;
+      rp->inc[C_S1] = (uint32_t)(d - 1);
+      rp->inc[C_S2] = (uint32_t)((D - 1) * spj);
+      rp->inc[C_AG] = (uint32_t)((D - 1) * spj);
+      rp->inc[C_S3] = (uint32_t)(d - 1);
+      break;
+    }
+    case OP_REDUCE_SCATTER:
+    case OP_ALL_GATHER: {
+      rp->partners = ((n == 32 ? 0u : (1u << n)) - 1u) & ~(1u << rank);
+      rp->inc[C_S1] = (uint32_t)(d - 1);
+      rp->inc[C_S2] = (uint32_t)(n - d);  // one piece from every other-domain rank
+      break;
+    }
+    case OP_BROADCAST: {
+      const int kr = t.rank_dom[root];
+      uint32_t cross = 0;
+      if (D > 1) {
+        if (k == kr) {  // my region's segments go to every other domain's owners
+          for (int s = j * spj; s < (j + 1) * spj; s++)
+            for (int q = 0; q < D; q++)
+              if (q != kr) cross |= 1u << owner_of(t, q, s);
+        } else {  // my region's segments come from root-domain owners
+          for (int s = j * spj; s < (j + 1) * spj; s++) cross |= 1u << owner_of(t, kr, s);
+        }
+      }
+      rp->partners = peers | cross;
+      rp->inc[C_S1] = (k == kr && rank != root) ? 1u : 0u;             // region from the root
+      rp->inc[C_S2] = (k != kr) ? (uint32_t)spj : 0u;                    // one signal per segment
+      rp->inc[C_S3] = (rank == root) ? 0u : (uint32_t)(d - 1);            // every peer's region but mine
+      break;
+    }
+    default:
+      break;
+  }
+  rp->inc[C_ACK] = (uint32_t)__builtin_popcount(rp->partners);
+}
+
+// Algorithmic bytes sent/received over the peer fabric by `rank` for one op, by walking the same
+// per-tile partition the kernels execute.
+void plan_bytes(const Topo& t, int op, int rank, int root, size_t count, int es, size_t tile, size_t* sent,
+                size_t* recv) {
+  *sent = *recv = 0;
+  if (count == 0 || t.n == 1 || tile == 0) return;
+  const int V = 16 / es;
+  const int k = t.rank_dom[rank], j = t.rank_idx[rank], d = t.dom_size[k], D = t.D, L = t.L, n = t.n;
+  Geometry g{tile, (count + tile - 1) / tile, 0};
+  size_t S = 0, R = 0;
+  for (size_t ti = 0; ti < g.ntiles; ti++) {
+    size_t len = std::min(g.tile, count - ti * g.tile);
+    auto seg = [&](int s) -> size_t { return s >= L ? len : floor_to(len * (size_t)s / L, V); };
+    auto piece = [&](int s, int p) -> size_t {
+      size_t b0 = seg(s), b1 = seg(s + 1);
+      return p >= D ? b1 : b0 + floor_to((b1 - b0) * (size_t)p / D, V);
+    };
+    auto region = [&](int q, int m) -> size_t {  // region length of member m of domain q
+      int sp = L / t.dom_size[q];
+      return seg((m + 1) * sp) - seg(m * sp);
+    };
+    auto sub = [&](size_t l, int dd, int i) -> size_t {  // piece i of dd of a shard tile of length l
+      size_t a = floor_to(l * (size_t)i / dd, V), b = (i + 1 >= dd) ? l : floor_to(l * (size_t)(i + 1) / dd, V);
+      return b - a;
+    };
+    if (op == OP_ALLREDUCE) {
+      const int spj = L / d;
+      for (int i = 0; i < d; i++)
+        if (i != j) {
+          S += region(k, i);  // S1 out
+          R += region(k, j);  // S1 in
+          S += region(k, j);  // S3 out
+          R += region(k, i);  // S3 in
+        }
+      for (int s = j * spj; s < (j + 1) * spj; s++)
+        for (int q = 0; q < D; q++)
+          if (q != k) {
+            S += piece(s, q + 1) - piece(s, q);  // partial piece out (S2)
+            R += piece(s, k + 1) - piece(s, k);  // partial in from domain q
+            S += piece(s, k + 1) - piece(s, k);  // reduced piece out to domain q (AG)
+            R += piece(s, q + 1) - piece(s, q);  // reduced piece in
+          }
+    } else if (op == OP_REDUCE_SCATTER || op == OP_ALL_GATHER) {
+      size_t reg = len;  // own shard + my piece of every other-domain shard
+      for (int r = 0; r < n; r++)
+        if (t.rank_dom[r] != k) reg += sub(len, d, j);
+      size_t intra_out = 0, intra_in = 0, cross_out = 0, cross_in = 0;
+      for (int i = 0; i < d; i++)
+        if (i != j) {
+          size_t regi = len;
+          for (int r = 0; r < n; r++)
+            if (t.rank_dom[r] != k) regi += sub(len, d, i);
+          intra_out += regi;  // RS: my data for peer i's region
+          intra_in += reg;    // RS: peer's data for my region
+        }
+      for (int r = 0; r < n; r++)
+        if (t.rank_dom[r] != k) {
+          cross_out += sub(len, d, j);  // RS: my partial piece of shard r to r
+        }
+      for (int q = 0; q < D; q++)
+        if (q != k)
+          for (int i = 0; i < t.dom_size[q]; i++) cross_in += sub(len, t.dom_size[q], i);  // = len per domain
+      if (op == OP_REDUCE_SCATTER) {
+        S += intra_out + cross_out;
+        R += intra_in + cross_in;
+      } else {  // AG is the mirror image
+        S += intra_in + cross_in;
+        R += intra_out + cross_out;
+      }
+    } else if (op == OP_BROADCAST) {
+      const int kr = t.rank_dom[root], spj = L / d;
+      if (rank == root)
+        for (int i = 0; i < d; i++)
+          if (i != j) S += region(k, i);  // B1
+      if (k == kr && rank != root) R += region(k, j);
+      if (D > 1) {
+        for (int s = j * spj; s < (j + 1) * spj; s++) {
+          size_t sl = seg(s + 1) - seg(s);
+          if (k == kr)
+            S += sl * (size_t)(D - 1);  // B2 out: each other domain gets segment s once
+          else
+            R += sl;
+        }
+      }
+      for (int i = 0; i < d; i++)
+        if (i != j) {  // B3: my region to peers (not to the root), peers' regions to me (not if root)
+          int peer = t.members[t.dom_first[k] + i];
+          if (peer != root) S += region(k, j);
+          if (rank != root) R += region(k, i);
+        }
+    }
+  }
+  *sent = S * (size_t)es;
+  *recv = R * (size_t)es;
+}
+
+}  // namespace hetccl

@@ -1,0 +1,498 @@
+// runtime.cu — host runtime behind include/hetccl.h: communicators (multi-process IPC bootstrap,
+// single-process multi-GPU, rank-multiplexed), argument validation and kernel launch. Every
+// data-moving step runs in kernels.cu; this file only allocates, maps and enqueues.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/hetccl.h"
+#include "hetccl_internal.h"
+
+namespace hetccl {
+cudaError_t launch_collective(const OpArgs& a, int nlocal, int dt, int red, bool cooperative, cudaStream_t s);
+cudaError_t launch_copy(const void* src, void* dst, size_t n, int es, cudaStream_t s);
+int max_coresident(int op, int dt, int red);
+}  // namespace hetccl
+
+using namespace hetccl;
+
+enum CommKind { KIND_PROC = 0, KIND_MUX = 1, KIND_ALL = 2 };
+
+struct hetcclComm {
+  int kind = KIND_PROC;
+  int n = 0, rank = 0, device = 0;
+  int map[kMaxRanks] = {0};
+  Topo topo{};
+  int nch_max = 32;
+  size_t slot_bytes = 0;
+  size_t alloc_bytes = 0;
+  char* local[kMaxRanks] = {nullptr};    // allocations owned by this comm (mux: one per rank)
+  char* mapped[kMaxRanks] = {nullptr};   // every rank's region as seen from this device
+  bool ipc_opened[kMaxRanks] = {false};  // mapped[r] came from cudaIpcOpenMemHandle
+  unsigned long long* err = nullptr;     // device error word
+  bool connected = false;
+  long long timeout_ns = 30LL * 1000000000LL;
+  std::string last_error;
+};
+
+namespace {
+
+struct Blob {
+  uint32_t magic;
+  int version;
+  int n, rank;
+  int map[kMaxRanks];
+  unsigned long long slot_bytes;
+  int nch_max;
+  int pad;
+  cudaIpcMemHandle_t handle;
+};
+static_assert(sizeof(Blob) <= HETCCL_BLOB_BYTES, "blob too large");
+constexpr uint32_t kMagic = 0x48435431u;  // "HCT1"
+
+hetcclResult_t fail(hetcclComm_t c, hetcclResult_t r, const char* fmt, ...) {
+  if (c) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    c->last_error = buf;
+  }
+  return r;
+}
+
+#define CUDA_TRY(c, call)                                                                                  \
+  do {                                                                                                     \
+    cudaError_t e_ = (call);                                                                               \
+    if (e_ != cudaSuccess) return fail((c), hetcclUnhandledCudaError, "%s: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+
+long env_long(const char* name, long dflt) {
+  const char* e = getenv(name);
+  return e && *e ? atol(e) : dflt;
+}
+
+void read_env(hetcclComm* c) {
+  c->nch_max = (int)std::max(1L, std::min((long)kMaxChannels, env_long("HETCCL_NCHANNELS", 32)));
+  c->slot_bytes = (size_t)std::max(64L, env_long("HETCCL_SLOT_KB", 2048)) * 1024;
+  c->slot_bytes = (c->slot_bytes + 255) / 256 * 256;
+  c->timeout_ns = (long long)std::max(1L, env_long("HETCCL_TIMEOUT_S", 30)) * 1000000000LL;
+  c->alloc_bytes = kFlagsReserve + (size_t)c->nch_max * kNumSlots * c->slot_bytes;
+}
+
+// allocate one rank's [flags | scratch] region on the current device, flags zeroed
+cudaError_t alloc_region(size_t bytes, char** out) {
+  cudaError_t e = cudaMalloc((void**)out, bytes);
+  if (e != cudaSuccess) return e;
+  return cudaMemset(*out, 0, kFlagsReserve);
+}
+
+struct DevGuard {
+  int prev = -1;
+  explicit DevGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+    else prev = -1;
+  }
+  ~DevGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+bool valid_dt(int dt) { return dt == DT_INT32 || dt == DT_F16 || dt == DT_F32 || dt == DT_BF16; }
+bool valid_red(int op) { return op == RED_SUM || op == RED_MAX || op == RED_MIN; }
+
+bool overlaps(const void* a, size_t an, const void* b, size_t bn) {
+  uintptr_t a0 = (uintptr_t)a, b0 = (uintptr_t)b;
+  return a0 < b0 + bn && b0 < a0 + an;
+}
+
+// NCCL in-place rules; returns nullptr if fine else a message
+const char* check_overlap(int op, const void* s, void* r, size_t count, int es, int rank, int n) {
+  const size_t b = count * (size_t)es;
+  switch (op) {
+    case OP_ALLREDUCE:
+    case OP_BROADCAST:
+      if (s && s != r && overlaps(s, b, r, b)) return "send and recv overlap (only sendbuf == recvbuf is allowed)";
+      return nullptr;
+    case OP_REDUCE_SCATTER:
+      if ((const char*)r == (const char*)s + (size_t)rank * b) return nullptr;
+      if (overlaps(s, b * n, r, b)) return "send and recv overlap (in place requires recvbuf == sendbuf + rank*recvcount)";
+      return nullptr;
+    case OP_ALL_GATHER:
+      if ((const char*)s == (const char*)r + (size_t)rank * b) return nullptr;
+      if (overlaps(s, b, r, b * n)) return "send and recv overlap (in place requires sendbuf == recvbuf + rank*sendcount)";
+      return nullptr;
+  }
+  return nullptr;
+}
+
+// the elements each rank's recvbuf holds for op (for the n == 1 copy)
+size_t recv_elems(int op, size_t count, int n) { return op == OP_ALL_GATHER ? count * n : count; }
+
+hetcclResult_t run_op(hetcclComm_t c, int op, const void* const* sends, void* const* recvs, size_t count, int dt,
+                      int red, int root, cudaStream_t stream) {
+  if (!c) return hetcclInvalidArgument;
+  if (!c->connected) return fail(c, hetcclInvalidUsage, "comm is not connected");
+  if (!valid_dt(dt)) return fail(c, hetcclInvalidArgument, "unknown dtype %d", dt);
+  if ((op == OP_ALLREDUCE || op == OP_REDUCE_SCATTER) && !valid_red(red))
+    return fail(c, hetcclInvalidArgument, "unknown reduction op %d", red);
+  if (op == OP_BROADCAST && (root < 0 || root >= c->n)) return fail(c, hetcclInvalidArgument, "root %d not in [0,%d)", root, c->n);
+  const int es = dtype_size(dt);
+  if (count > ((size_t)1 << 62) / (size_t)es / (size_t)c->n) return fail(c, hetcclInvalidArgument, "count too large");
+  if (count == 0) return hetcclSuccess;
+  const int nlocal = c->kind == KIND_MUX ? c->n : 1;
+  for (int i = 0; i < nlocal; i++) {
+    const int r = c->kind == KIND_MUX ? i : c->rank;
+    const bool need_send = !(op == OP_BROADCAST && r != root);
+    if ((need_send && !sends[i]) || !recvs[i]) return fail(c, hetcclInvalidArgument, "null buffer for rank %d", r);
+    const char* msg = check_overlap(op, sends[i], recvs[i], count, es, r, c->n);
+    if (msg) return fail(c, hetcclInvalidArgument, "rank %d: %s", r, msg);
+  }
+  DevGuard g(c->device);
+  if (c->n == 1) {  // a9: recv <- send
+    CUDA_TRY(c, launch_copy(sends[0], recvs[0], recv_elems(op, count, 1), es, stream));
+    return hetcclSuccess;
+  }
+  OpArgs a;
+  memset(&a, 0, sizeof(a));
+  a.topo = c->topo;
+  for (int r = 0; r < c->n; r++) {
+    a.mem[r].flags = (uint64_t*)c->mapped[r];
+    a.mem[r].scratch = c->mapped[r] + kFlagsReserve;
+    make_rank_plan(c->topo, op, r, root, &a.rp[r]);
+  }
+  for (int i = 0; i < nlocal; i++) {
+    a.send[i] = sends[i];
+    a.recv[i] = recvs[i];
+    a.local_rank[i] = c->kind == KIND_MUX ? i : c->rank;
+  }
+  int nch_max = c->nch_max;
+  if (c->kind == KIND_MUX) {
+    int cap = max_coresident(op, dt, red);
+    if (cap < nlocal) return fail(c, hetcclInternalError, "device cannot co-schedule %d ranks", nlocal);
+    nch_max = std::min(nch_max, cap / nlocal);
+  }
+  const size_t slot_elems = c->slot_bytes / (size_t)es;
+  Geometry geo = make_geometry(c->topo, op, count, es, nch_max, slot_elems);
+  if (slot_mult_num(c->topo, op, geo.tile) > slot_elems)
+    return fail(c, hetcclInternalError, "scratch slot too small for this domain map (raise HETCCL_SLOT_KB)");
+  a.count = count;
+  a.tile = geo.tile;
+  a.ntiles = geo.ntiles;
+  a.nch = geo.nch;
+  a.slot_elems = slot_elems;
+  a.root = root;
+  a.op = op;
+  a.err = c->err;
+  a.timeout_ns = c->timeout_ns;
+  CUDA_TRY(c, launch_collective(a, nlocal, dt, red, c->kind == KIND_MUX, stream));
+  return hetcclSuccess;
+}
+
+hetcclResult_t init_common(hetcclComm* c, int n, const int* map) {
+  if (build_topo(n, map, &c->topo)) return hetcclInvalidArgument;
+  c->n = n;
+  memcpy(c->map, map, sizeof(int) * n);
+  read_env(c);
+  return hetcclSuccess;
+}
+
+}  // namespace
+
+extern "C" {
+
+hetcclResult_t hetccl_get_version(int* version) {
+  if (!version) return hetcclInvalidArgument;
+  *version = HETCCL_VERSION;
+  return hetcclSuccess;
+}
+
+hetcclResult_t hetccl_validate_map(int nranks, const int* rank_to_domain, int* ndomains) {
+  Topo t;
+  if (build_topo(nranks, rank_to_domain, &t)) return hetcclInvalidArgument;
+  if (ndomains) *ndomains = t.D;
+  return hetcclSuccess;
+}
+
+hetcclResult_t hetccl_comm_init(hetcclComm_t* comm, int nranks, int rank, const int* rank_to_domain,
+                                int cuda_device) {
+  if (!comm) return hetcclInvalidArgument;
+  *comm = nullptr;
+  if (rank < 0 || rank >= nranks) return hetcclInvalidArgument;
+  hetcclComm* c = new hetcclComm();
+  if (init_common(c, nranks, rank_to_domain) != hetcclSuccess) {
+    delete c;
+    return hetcclInvalidArgument;
+  }
+  c->kind = KIND_PROC;
+  c->rank = rank;
+  c->device = cuda_device;
+  DevGuard g(cuda_device);
+  cudaError_t e = alloc_region(c->alloc_bytes, &c->local[0]);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&c->err, sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemset(c->err, 0, sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    if (c->local[0]) cudaFree(c->local[0]);
+    delete c;
+    return hetcclUnhandledCudaError;
+  }
+  c->mapped[rank] = c->local[0];
+  if (nranks == 1) c->connected = true;
+  *comm = c;
+  return hetcclSuccess;
+}
+
+hetcclResult_t hetccl_comm_export(hetcclComm_t c, void* blob, size_t* blob_bytes) {
+  if (!c || !blob || !blob_bytes) return hetcclInvalidArgument;
+  if (c->kind != KIND_PROC) return fail(c, hetcclInvalidUsage, "export is for one-rank-per-process comms");
+  if (*blob_bytes < HETCCL_BLOB_BYTES) return fail(c, hetcclInvalidArgument, "blob buffer < HETCCL_BLOB_BYTES");
+  Blob b;
+  memset(&b, 0, sizeof(b));
+  b.magic = kMagic;
+  b.version = HETCCL_VERSION;
+  b.n = c->n;
+  b.rank = c->rank;
+  memcpy(b.map, c->map, sizeof(int) * c->n);
+  b.slot_bytes = c->slot_bytes;
+  b.nch_max = c->nch_max;
+  DevGuard g(c->device);
+  CUDA_TRY(c, cudaIpcGetMemHandle(&b.handle, c->local[0]));
+  memset(blob, 0, HETCCL_BLOB_BYTES);
+  memcpy(blob, &b, sizeof(b));
+  *blob_bytes = HETCCL_BLOB_BYTES;
+  return hetcclSuccess;
+}
+
+hetcclResult_t hetccl_comm_connect(hetcclComm_t c, const void* blobs, size_t blob_bytes) {
+  if (!c || !blobs) return hetcclInvalidArgument;
+  if (c->kind != KIND_PROC) return fail(c, hetcclInvalidUsage, "connect is for one-rank-per-process comms");
+  if (c->connected) return hetcclSuccess;
+  if (blob_bytes != (size_t)c->n * HETCCL_BLOB_BYTES)
+    return fail(c, hetcclInvalidArgument, "expected %d blobs of %d bytes", c->n, HETCCL_BLOB_BYTES);
+  DevGuard g(c->device);
+  for (int r = 0; r < c->n; r++) {
+    Blob b;
+    memcpy(&b, (const char*)blobs + (size_t)r * HETCCL_BLOB_BYTES, sizeof(b));
+    if (b.magic != kMagic || b.version != HETCCL_VERSION || b.n != c->n || b.rank != r)
+      return fail(c, hetcclInvalidUsage, "blob %d is not a hetccl blob for rank %d of %d", r, r, c->n);
+    if (memcmp(b.map, c->map, sizeof(int) * c->n) != 0)
+      return fail(c, hetcclInvalidUsage, "rank %d passed a different rank_to_domain map", r);
+    if (b.slot_bytes != c->slot_bytes || b.nch_max != c->nch_max)
+      return fail(c, hetcclInvalidUsage, "rank %d has different HETCCL_SLOT_KB/HETCCL_NCHANNELS", r);
+    if (r == c->rank) continue;
+    void* p = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&p, b.handle, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return fail(c, hetcclSystemError, "cudaIpcOpenMemHandle(rank %d): %s", r, cudaGetErrorString(e));
+    c->mapped[r] = (char*)p;
+    c->ipc_opened[r] = true;
+  }
+  c->connected = true;
+  return hetcclSuccess;
+}
+
+hetcclResult_t hetccl_comm_init_all(hetcclComm_t* comms, int ndev, const int* devlist, const int* rank_to_domain) {
+  if (!comms || !devlist || ndev < 1) return hetcclInvalidArgument;
+  Topo t;
+  if (build_topo(ndev, rank_to_domain, &t)) return hetcclInvalidArgument;
+  for (int i = 0; i < ndev; i++)
+    for (int j = 0; j < i; j++)
+      if (devlist[i] == devlist[j]) return hetcclInvalidArgument;  // one rank per device (use mux otherwise)
+  hetcclComm* cs[kMaxRanks] = {nullptr};
+  int prev;
+  cudaGetDevice(&prev);
+  hetcclResult_t res = hetcclSuccess;
+  for (int i = 0; i < ndev && res == hetcclSuccess; i++) {
+    cs[i] = new hetcclComm();
+    init_common(cs[i], ndev, rank_to_domain);
+    cs[i]->kind = KIND_ALL;
+    cs[i]->rank = i;
+    cs[i]->device = devlist[i];
+    if (cudaSetDevice(devlist[i]) != cudaSuccess || alloc_region(cs[i]->alloc_bytes, &cs[i]->local[0]) != cudaSuccess ||
+        cudaMalloc((void**)&cs[i]->err, 8) != cudaSuccess || cudaMemset(cs[i]->err, 0, 8) != cudaSuccess)
+      res = hetcclUnhandledCudaError;
+    for (int j = 0; j < ndev && res == hetcclSuccess; j++) {
+      if (j == i) continue;
+      int can = 0;
+      cudaDeviceCanAccessPeer(&can, devlist[i], devlist[j]);
+      if (!can) res = hetcclSystemError;
+      cudaError_t e = cudaDeviceEnablePeerAccess(devlist[j], 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+      else if (e != cudaSuccess) res = hetcclUnhandledCudaError;
+    }
+    if (cudaDeviceSynchronize() != cudaSuccess) res = hetcclUnhandledCudaError;
+  }
+  if (res == hetcclSuccess) {
+    for (int i = 0; i < ndev; i++) {
+      for (int r = 0; r < ndev; r++) cs[i]->mapped[r] = cs[r]->local[0];
+      cs[i]->connected = true;
+      comms[i] = cs[i];
+    }
+  } else {
+    for (int i = 0; i < ndev; i++)
+      if (cs[i]) {
+        cudaSetDevice(devlist[i]);
+        if (cs[i]->local[0]) cudaFree(cs[i]->local[0]);
+        if (cs[i]->err) cudaFree(cs[i]->err);
+        delete cs[i];
+      }
+  }
+  cudaSetDevice(prev);
+  return res;
+}
+
+hetcclResult_t hetccl_comm_init_mux(hetcclComm_t* comm, int nranks, const int* rank_to_domain, int cuda_device) {
+  if (!comm) return hetcclInvalidArgument;
+  *comm = nullptr;
+  hetcclComm* c = new hetcclComm();
+  if (init_common(c, nranks, rank_to_domain) != hetcclSuccess) {
+    delete c;
+    return hetcclInvalidArgument;
+  }
+  c->kind = KIND_MUX;
+  c->device = cuda_device;
+  DevGuard g(cuda_device);
+  cudaError_t e = cudaSuccess;
+  for (int r = 0; r < nranks && e == cudaSuccess; r++) e = alloc_region(c->alloc_bytes, &c->local[r]);
+  if (e == cudaSuccess) e = cudaMalloc((void**)&c->err, 8);
+  if (e == cudaSuccess) e = cudaMemset(c->err, 0, 8);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    for (int r = 0; r < nranks; r++)
+      if (c->local[r]) cudaFree(c->local[r]);
+    if (c->err) cudaFree(c->err);
+    delete c;
+    return hetcclUnhandledCudaError;
+  }
+  for (int r = 0; r < nranks; r++) c->mapped[r] = c->local[r];
+  c->connected = true;
+  *comm = c;
+  return hetcclSuccess;
+}
+
+hetcclResult_t hetccl_comm_destroy(hetcclComm_t c) {
+  if (!c) return hetcclInvalidArgument;
+  {
+    DevGuard g(c->device);
+    cudaDeviceSynchronize();
+    for (int r = 0; r < kMaxRanks; r++) {
+      if (c->ipc_opened[r]) cudaIpcCloseMemHandle(c->mapped[r]);
+      if (c->local[r]) cudaFree(c->local[r]);
+    }
+    if (c->err) cudaFree(c->err);
+  }
+  delete c;
+  return hetcclSuccess;
+}
+
+hetcclResult_t hetccl_comm_info(hetcclComm_t c, int* rank, int* nranks, int* domain, int* ndomains, int* domain_rank,
+                                int* domain_size) {
+  if (!c) return hetcclInvalidArgument;
+  if (rank) *rank = c->rank;
+  if (nranks) *nranks = c->n;
+  if (domain) *domain = c->topo.rank_dom[c->rank];
+  if (ndomains) *ndomains = c->topo.D;
+  if (domain_rank) *domain_rank = c->topo.rank_idx[c->rank];
+  if (domain_size) *domain_size = c->topo.dom_size[c->topo.rank_dom[c->rank]];
+  return hetcclSuccess;
+}
+
+hetcclResult_t hetccl_comm_get_async_error(hetcclComm_t c) {
+  if (!c) return hetcclInvalidArgument;
+  unsigned long long v = 0;
+  DevGuard g(c->device);
+  CUDA_TRY(c, cudaMemcpy(&v, c->err, sizeof(v), cudaMemcpyDeviceToHost));
+  if (v) return fail(c, hetcclInternalError, "device-side timeout waiting on counter %llu", v >> 8);
+  return hetcclSuccess;
+}
+
+const char* hetccl_get_error_string(hetcclResult_t r) {
+  switch (r) {
+    case hetcclSuccess: return "no error";
+    case hetcclUnhandledCudaError: return "unhandled cuda error";
+    case hetcclSystemError: return "system error (IPC / host)";
+    case hetcclInternalError: return "internal error (device timeout or protocol failure)";
+    case hetcclInvalidArgument: return "invalid argument";
+    case hetcclInvalidUsage: return "invalid usage";
+  }
+  return "unknown result code";
+}
+
+const char* hetccl_get_last_error(hetcclComm_t c) { return c ? c->last_error.c_str() : "null comm"; }
+
+hetcclResult_t hetccl_allreduce(const void* sendbuf, void* recvbuf, size_t count, hetcclDataType_t dt,
+                                hetcclRedOp_t op, hetcclComm_t comm, hetcclStream_t stream) {
+  if (comm && comm->kind == KIND_MUX) return fail(comm, hetcclInvalidUsage, "use hetccl_mux_* on a mux comm");
+  return run_op(comm, OP_ALLREDUCE, &sendbuf, &recvbuf, count, dt, op, 0, (cudaStream_t)stream);
+}
+hetcclResult_t hetccl_reduce_scatter(const void* sendbuf, void* recvbuf, size_t recvcount, hetcclDataType_t dt,
+                                     hetcclRedOp_t op, hetcclComm_t comm, hetcclStream_t stream) {
+  if (comm && comm->kind == KIND_MUX) return fail(comm, hetcclInvalidUsage, "use hetccl_mux_* on a mux comm");
+  return run_op(comm, OP_REDUCE_SCATTER, &sendbuf, &recvbuf, recvcount, dt, op, 0, (cudaStream_t)stream);
+}
+hetcclResult_t hetccl_all_gather(const void* sendbuf, void* recvbuf, size_t sendcount, hetcclDataType_t dt,
+                                 hetcclComm_t comm, hetcclStream_t stream) {
+  if (comm && comm->kind == KIND_MUX) return fail(comm, hetcclInvalidUsage, "use hetccl_mux_* on a mux comm");
+  return run_op(comm, OP_ALL_GATHER, &sendbuf, &recvbuf, sendcount, dt, RED_SUM, 0, (cudaStream_t)stream);
+}
+hetcclResult_t hetccl_broadcast(const void* sendbuf, void* recvbuf, size_t count, hetcclDataType_t dt, int root,
+                                hetcclComm_t comm, hetcclStream_t stream) {
+  if (comm && comm->kind == KIND_MUX) return fail(comm, hetcclInvalidUsage, "use hetccl_mux_* on a mux comm");
+  return run_op(comm, OP_BROADCAST, &sendbuf, &recvbuf, count, dt, RED_SUM, root, (cudaStream_t)stream);
+}
+
+static hetcclResult_t mux_check(hetcclComm_t c, const void* a, const void* b) {
+  if (!c || !a || !b) return hetcclInvalidArgument;
+  if (c->kind != KIND_MUX) return fail(c, hetcclInvalidUsage, "hetccl_mux_* needs a comm from hetccl_comm_init_mux");
+  return hetcclSuccess;
+}
+hetcclResult_t hetccl_mux_allreduce(const void* const* s, void* const* r, size_t count, hetcclDataType_t dt,
+                                    hetcclRedOp_t op, hetcclComm_t c, hetcclStream_t stream) {
+  hetcclResult_t e = mux_check(c, s, r);
+  return e ? e : run_op(c, OP_ALLREDUCE, s, r, count, dt, op, 0, (cudaStream_t)stream);
+}
+hetcclResult_t hetccl_mux_reduce_scatter(const void* const* s, void* const* r, size_t recvcount, hetcclDataType_t dt,
+                                         hetcclRedOp_t op, hetcclComm_t c, hetcclStream_t stream) {
+  hetcclResult_t e = mux_check(c, s, r);
+  return e ? e : run_op(c, OP_REDUCE_SCATTER, s, r, recvcount, dt, op, 0, (cudaStream_t)stream);
+}
+hetcclResult_t hetccl_mux_all_gather(const void* const* s, void* const* r, size_t sendcount, hetcclDataType_t dt,
+                                     hetcclComm_t c, hetcclStream_t stream) {
+  hetcclResult_t e = mux_check(c, s, r);
+  return e ? e : run_op(c, OP_ALL_GATHER, s, r, sendcount, dt, RED_SUM, 0, (cudaStream_t)stream);
+}
+hetcclResult_t hetccl_mux_broadcast(const void* const* s, void* const* r, size_t count, hetcclDataType_t dt, int root,
+                                    hetcclComm_t c, hetcclStream_t stream) {
+  hetcclResult_t e = mux_check(c, s, r);
+  return e ? e : run_op(c, OP_BROADCAST, s, r, count, dt, RED_SUM, root, (cudaStream_t)stream);
+}
+
+hetcclResult_t hetccl_plan_info(int nranks, const int* rank_to_domain, int rank, int op, size_t count,
+                                hetcclDataType_t dt, int root, int nchannels, hetcclPlanInfo_t* info) {
+  Topo t;
+  if (!info || build_topo(nranks, rank_to_domain, &t) || rank < 0 || rank >= nranks || op < 0 || op > 3 ||
+      !valid_dt(dt) || (op == OP_BROADCAST && (root < 0 || root >= nranks)))
+    return hetcclInvalidArgument;
+  hetcclComm tmp;
+  read_env(&tmp);
+  const int es = dtype_size(dt);
+  const int nch = nchannels > 0 ? std::min(nchannels, kMaxChannels) : tmp.nch_max;
+  Geometry g = make_geometry(t, op, count, es, nch, tmp.slot_bytes / es);
+  memset(info, 0, sizeof(*info));
+  plan_bytes(t, op, rank, root, count, es, g.tile, &info->bytes_sent, &info->bytes_recv);
+  info->tile_elems = g.tile;
+  info->ntiles = g.ntiles;
+  info->nchannels = g.nch;
+  info->nslots = kNumSlots;
+  return hetcclSuccess;
+}
+
+}  // extern "C"

@@ -1,0 +1,139 @@
+"""CPU-side checks of the C ABI (tests -m "not gpu"): the library loads without a GPU, exports every
+symbol include/hetccl.h declares, validates maps, and its plan's per-rank byte counts equal the
+closed forms of SURVEY §8(d) (no compute calls)."""
+import ctypes
+import os
+import re
+from fractions import Fraction
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def hc():
+    from paper_2601_22585_b200 import build
+    build.build()
+    import paper_2601_22585_b200 as hc
+    return hc
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "hetccl.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(hetccl_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_exports_every_declared_symbol(hc):
+    lib = hc.lib()
+    declared = _declared()
+    assert len(declared) >= 20
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert set(declared) == set(hc.EXPORTED)
+
+
+def test_version_and_error_strings(hc):
+    v = ctypes.c_int()
+    assert hc.lib().hetccl_get_version(ctypes.byref(v)) == 0 and v.value == 100
+    for code in range(6):
+        assert hc.lib().hetccl_get_error_string(code)
+
+
+@pytest.mark.parametrize("m,D", [([0, 1], 2), ([0, 0, 1, 1, 2, 2, 2, 2], 3), ([1, 0], 2), ([0] * 16, 1)])
+def test_validate_map_ok(hc, m, D):
+    assert hc.hetccl_validate_map(m) == D
+
+
+@pytest.mark.parametrize("m", [[1, 1], [0, 2], [-1, 0], [0] * 17, []])
+def test_validate_map_rejects(hc, m):
+    with pytest.raises(hc.HetcclError):
+        if not m:
+            hc._check(hc.lib().hetccl_validate_map(0, None, None))
+        else:
+            hc.hetccl_validate_map(m)
+
+
+def test_null_and_bad_args_without_gpu(hc):
+    lib = hc.lib()
+    assert lib.hetccl_allreduce(None, None, 4, 9, 0, None, None) == 4  # null comm
+    info = hc.PlanInfo()
+    assert lib.hetccl_plan_info(2, hc._imap([0, 1]), 0, 9, 16, 9, 0, 0, ctypes.byref(info)) == 4  # bad op
+    assert lib.hetccl_plan_info(2, hc._imap([0, 1]), 0, 0, 16, 5, 0, 0, ctypes.byref(info)) == 4  # bad dtype
+    assert lib.hetccl_plan_info(2, hc._imap([0, 1]), 0, 3, 16, 9, 2, 0, ctypes.byref(info)) == 4  # bad root
+
+
+SPLITS = {"1+1": [0, 1], "2+2": [0, 0, 1, 1], "1+3": [0, 1, 1, 1], "1+1+2": [0, 1, 2, 2],
+          "4+4": [0] * 4 + [1] * 4, "2+6": [0, 0] + [1] * 6, "2+2+4": [0, 0, 1, 1, 2, 2, 2, 2], "8": [0] * 8}
+
+
+@pytest.mark.parametrize("name", sorted(SPLITS))
+def test_allreduce_bytes_closed_form(hc, name):
+    """Per-rank AR bytes = S*(2(d-1)/d + 2(D-1)/(D d)) for a count divisible by everything."""
+    m = SPLITS[name]
+    n, D = len(m), max(m) + 1
+    count = 8 * 840 * 64 * 1024  # divisible by every L*D*V here
+    S = count * 2
+    busiest = 0
+    for r in range(n):
+        d = m.count(m[r])
+        want = S * (Fraction(2 * (d - 1), d) + Fraction(2 * (D - 1), D * d))
+        info = hc.hetccl_plan_info(m, r, hc.OP_ALLREDUCE, count, hc.BFLOAT16)
+        assert info["bytes_sent"] == want and info["bytes_recv"] == want, (r, info, want)
+        busiest = max(busiest, want)
+    flat = Fraction(2 * (n - 1), n) * S
+    table = {"1+1": 1, "2+2": 1, "1+3": Fraction(9, 10), "1+1+2": Fraction(9, 10), "4+4": 1,
+             "2+6": Fraction(21, 22), "2+2+4": Fraction(21, 22), "8": 1}
+    assert flat / busiest == table[name]
+
+
+@pytest.mark.parametrize("name", ["2+6", "4+4", "1+3", "2+2+4"])
+def test_rs_ag_bytes_closed_form(hc, name):
+    """RS received per rank = (d-1)/d*S + (D-1)*S/n; AG is the mirror (sent = that); SURVEY §8(d)."""
+    m = SPLITS[name]
+    n, D = len(m), max(m) + 1
+    R = 840 * 64 * 1024  # recvcount
+    S = n * R * 2
+    for r in range(n):
+        d = m.count(m[r])
+        recv = S * (Fraction(d - 1, d) + Fraction(D - 1, n))
+        sent = S * Fraction(n - 1, n)
+        rs = hc.hetccl_plan_info(m, r, hc.OP_REDUCE_SCATTER, R, hc.BFLOAT16)
+        ag = hc.hetccl_plan_info(m, r, hc.OP_ALL_GATHER, R, hc.BFLOAT16)
+        assert rs["bytes_recv"] == recv and rs["bytes_sent"] == sent, (r, rs)
+        assert ag["bytes_sent"] == recv and ag["bytes_recv"] == sent, (r, ag)
+
+
+def test_rs_2p6_survey_numbers(hc):
+    """C3 (2+6): 2-domain ranks receive 0.625 S, 6-domain ranks 0.958 S."""
+    m = SPLITS["2+6"]
+    R = 16777216
+    S = 8 * R * 2
+    r0 = hc.hetccl_plan_info(m, 0, hc.OP_REDUCE_SCATTER, R, hc.BFLOAT16)["bytes_recv"]
+    r7 = hc.hetccl_plan_info(m, 7, hc.OP_REDUCE_SCATTER, R, hc.BFLOAT16)["bytes_recv"]
+    assert abs(r0 / S - 5 / 8) < 1e-4  # 16-byte rounding of the 1/6 pieces moves a few bytes
+    assert abs(r7 / S - 23 / 24) < 1e-4
+
+
+def test_conservation(hc):
+    """Bytes sent over all ranks == bytes received over all ranks, any op, ragged counts."""
+    for name, m in SPLITS.items():
+        for op in range(4):
+            for count in (1, 999, 123457):
+                s = sum(hc.hetccl_plan_info(m, r, op, count, hc.BFLOAT16, root=len(m) - 1)["bytes_sent"]
+                        for r in range(len(m)))
+                v = sum(hc.hetccl_plan_info(m, r, op, count, hc.BFLOAT16, root=len(m) - 1)["bytes_recv"]
+                        for r in range(len(m)))
+                assert s == v, (name, op, count)
+
+
+def test_single_domain_has_no_cross_traffic_and_singletons_no_intra(hc):
+    """SPEC.md:400 analog: one domain -> only intra bytes (flat 2(n-1)/n S); all-singleton domains ->
+    only the cross exchange (2(D-1)/D S)."""
+    count = 8 * 840 * 64
+    S = count * 4
+    one = hc.hetccl_plan_info([0] * 4, 0, hc.OP_ALLREDUCE, count, hc.FLOAT32)
+    assert one["bytes_sent"] == S * 3 // 2
+    sing = hc.hetccl_plan_info([0, 1, 2, 3], 0, hc.OP_ALLREDUCE, count, hc.FLOAT32)
+    assert sing["bytes_sent"] == S * 3 // 2

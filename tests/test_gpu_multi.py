@@ -1,0 +1,93 @@
+"""GPU parity, one rank per GPU (single process driving 2 or 4 B200s over NVLink peer access via
+hetccl_comm_init_all): each rank's kernel runs on its own GPU and pushes into peers' scratch over
+NVSwitch. Compared element by element with the oracle."""
+import numpy as np
+import pytest
+
+import oracle
+from harness import MAPS, assert_matches, inputs, to_numpy, to_torch
+
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+
+
+@pytest.fixture(autouse=True)
+def _env(monkeypatch):
+    monkeypatch.setenv("HETCCL_TIMEOUT_S", "10")
+
+
+def _ngpu():
+    import torch
+    return torch.cuda.device_count()
+
+
+def _comms(m):
+    import paper_2601_22585_b200 as hc
+    return hc.hetccl_comm_init_all(list(range(len(m))), m)
+
+
+def _streams(n):
+    import torch
+    return [torch.cuda.Stream(device=i) for i in range(n)]
+
+
+def _sync(n):
+    import torch
+    for i in range(n):
+        torch.cuda.synchronize(i)
+
+
+MULTI_MAPS = ["1+1", "2", "2+2", "1+3", "1+1+2", "4", "singletons4"]
+
+
+@pytest.mark.parametrize("name", MULTI_MAPS)
+@pytest.mark.parametrize("dt,op", [("bf16", "sum"), ("f32", "sum"), ("int32", "sum"), ("f16", "max")])
+def test_allreduce_multi(name, dt, op, monkeypatch):
+    import paper_2601_22585_b200 as hc
+    m = MAPS[name]
+    n = len(m)
+    if _ngpu() < n:
+        pytest.skip(f"needs {n} GPUs")
+    monkeypatch.setenv("HETCCL_TILE_KB", "16")
+    count = 5 * 8192 + 333
+    xs = inputs("bits" if dt == "int32" else "normal", 11, n, count, dt)
+    comms = _comms(m)
+    try:
+        ss = _streams(n)
+        sends = [to_torch(xs[r], dt, f"cuda:{r}") for r in range(n)]
+        recvs = [s.clone().fill_(0) for s in sends]
+        _sync(n)
+        for r in range(n):
+            hc.allreduce(sends[r], recvs[r], comms[r], op=op, stream=ss[r])
+        _sync(n)
+        for r in range(n):
+            hc.hetccl_comm_get_async_error(comms[r])
+        want = oracle.allreduce(xs, m, dt, op)
+        for r in range(n):
+            assert_matches(to_numpy(recvs[r], dt), want, xs, dt, op, f"{name} rank {r}")
+    finally:
+        for c in comms:
+            hc.hetccl_comm_destroy(c)
+
+
+def test_c1_fp32_1mi_bitexact():
+    """BASELINE config 0 on two real GPUs: fp32 sum, 1 Mi elements, 1+1 — bit-exact vs the oracle."""
+    import paper_2601_22585_b200 as hc
+    if _ngpu() < 2:
+        pytest.skip("needs 2 GPUs")
+    m = MAPS["1+1"]
+    for kind in ("uniform", "ramp"):
+        xs = inputs(kind, 1, 2, 1 << 20, "f32")
+        comms = _comms(m)
+        try:
+            sends = [to_torch(xs[r], "f32", f"cuda:{r}") for r in range(2)]
+            recvs = [s.clone() for s in sends]
+            for r in range(2):
+                with __import__("torch").cuda.device(r):
+                    hc.allreduce(sends[r], recvs[r], comms[r])
+            _sync(2)
+            want = oracle.allreduce(xs, m, "f32", "sum")
+            for r in range(2):
+                np.testing.assert_array_equal(to_numpy(recvs[r], "f32").view(np.uint32), want.view(np.uint32))
+        finally:
+            for c in comms:
+                hc.hetccl_comm_destroy(c)

@@ -1,0 +1,114 @@
+"""GPU parity, rank-multiplexed mode: every logical rank of an n-rank domain split runs
+inside ONE cooperative kernel on one B200, through the C ABI (hetccl_mux_*), with the same device
+code and flag protocol as the one-rank-per-GPU path. Compared element by element with the oracle."""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from harness import MAPS, assert_matches, inputs, to_numpy, to_torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(autouse=True)
+def _env(monkeypatch):
+    monkeypatch.setenv("HETCCL_TIMEOUT_S", "10")
+
+
+def _hc():
+    import paper_2601_22585_b200 as hc
+    return hc
+
+
+def _run_ar(name, dt, op, count, tile_kb=None, nch=None, kind="normal", seed=1, inplace=False, monkeypatch=None):
+    import torch
+    hc = _hc()
+    if tile_kb:
+        monkeypatch.setenv("HETCCL_TILE_KB", str(tile_kb))
+    if nch:
+        monkeypatch.setenv("HETCCL_NCHANNELS", str(nch))
+    m = MAPS[name]
+    n = len(m)
+    xs = inputs(kind, seed, n, count, dt)
+    comm = hc.hetccl_comm_init_mux(n, m, 0)
+    try:
+        sends = [to_torch(x, dt, "cuda") for x in xs]
+        recvs = sends if inplace else [torch.full_like(s, 7) for s in sends]
+        hc.mux_allreduce(sends, recvs, comm, op=op)
+        torch.cuda.synchronize()
+        hc.hetccl_comm_get_async_error(comm)
+        want = oracle.allreduce(xs, m, dt, op)
+        for r in range(n):
+            assert_matches(to_numpy(recvs[r], dt), want, xs, dt, op, f"{name} {dt} {op} rank {r}")
+    finally:
+        hc.hetccl_comm_destroy(comm)
+
+
+@pytest.mark.parametrize("name", ["1+1", "2+2", "1+3", "1+1+2", "4+4", "2+6", "2+2+4", "8", "singletons4",
+                                  "interleaved", "3+5", "1+2+3"])
+@pytest.mark.parametrize("dt", ["f32", "bf16"])
+def test_allreduce_splits(name, dt, monkeypatch):
+    # 4 KiB tiles -> many tiles per channel, ragged last tile (count not a multiple of anything)
+    _run_ar(name, dt, "sum", 3 * 4096 + 1000 + 3, tile_kb=4, monkeypatch=monkeypatch)
+
+
+@pytest.mark.parametrize("dt", ["int32", "f16", "f32", "bf16"])
+@pytest.mark.parametrize("op", ["sum", "max", "min"])
+def test_allreduce_dtypes_ops(dt, op, monkeypatch):
+    _run_ar("2+2+4", dt, op, 20000 + 13, tile_kb=8, kind="bits" if dt == "int32" else "normal", seed=3,
+            monkeypatch=monkeypatch)
+
+
+@pytest.mark.parametrize("count", [1, 2, 7, 8, 9, 63, 1000, 65536 + 5])
+def test_allreduce_small_and_ragged(count, monkeypatch):
+    _run_ar("2+6", "bf16", "sum", count, monkeypatch=monkeypatch)
+    _run_ar("1+1", "f32", "sum", count, monkeypatch=monkeypatch)
+
+
+def test_allreduce_inplace(monkeypatch):
+    _run_ar("4+4", "bf16", "sum", 100003, tile_kb=16, inplace=True, monkeypatch=monkeypatch)
+
+
+def test_allreduce_c1_config(monkeypatch):
+    """BASELINE config 0: fp32 sum of 1 Mi elements over 2 ranks as 1+1 (ramp and uniform data)."""
+    _run_ar("1+1", "f32", "sum", 1 << 20, kind="uniform", seed=1, monkeypatch=monkeypatch)
+    _run_ar("1+1", "f32", "sum", 1 << 20, kind="ramp", monkeypatch=monkeypatch)
+
+
+def test_repeated_calls_and_channel_changes(monkeypatch):
+    """Counters are cumulative across launches: vary count/tile/channels between calls on one comm."""
+    import torch
+    hc = _hc()
+    m = MAPS["2+2+4"]
+    n = len(m)
+    comm = hc.hetccl_comm_init_mux(n, m, 0)
+    try:
+        for it, (count, tkb) in enumerate([(5000, 4), (100000, 16), (17, 4), (300000, 64), (5000, 4)] * 3):
+            monkeypatch.setenv("HETCCL_TILE_KB", str(tkb))
+            xs = inputs("normal", 100 + it, n, count, "bf16")
+            sends = [to_torch(x, "bf16", "cuda") for x in xs]
+            recvs = [torch.empty_like(s) for s in sends]
+            hc.mux_allreduce(sends, recvs, comm)
+            torch.cuda.synchronize()
+            want = oracle.allreduce(xs, m, "bf16", "sum")
+            for r in range(n):
+                assert_matches(to_numpy(recvs[r], "bf16"), want, xs, "bf16", "sum", f"iter {it} rank {r}")
+        hc.hetccl_comm_get_async_error(comm)
+    finally:
+        hc.hetccl_comm_destroy(comm)
+
+
+def test_n1_copy():
+    import torch
+    hc = _hc()
+    comm = hc.hetccl_comm_init_mux(1, [0], 0)
+    try:
+        x = torch.randn(12345, device="cuda")
+        y = torch.empty_like(x)
+        hc.mux_allreduce([x], [y], comm)
+        torch.cuda.synchronize()
+        assert torch.equal(x, y)
+    finally:
+        hc.hetccl_comm_destroy(comm)
