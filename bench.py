@@ -1,0 +1,415 @@
+#!/usr/bin/env python
+"""bench.py — hierarchical All-Reduce bus bandwidth on B200 (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl hetccl|reference] [--mib 256]
+
+One "step" = one hierarchical All-Reduce (intra-domain RS -> cross-domain
+exchange -> intra-domain AG, one kernel launch) of a 256 MiB bf16 gradient bucket per rank.
+* N = 1: the BASELINE configs[1] target point (4+4 domains, 8 ranks, 256 MiB bf16) with all 8 logical
+  ranks multiplexed on one B200 (hetccl_comm_init_mux: same kernel, one cooperative launch); every
+  "NVLink" byte is local HBM traffic, so the roofline is HBM.
+* N > 1 (torchrun, one process per GPU, NCCL process group for barriers/timing only): real NVLink 5
+  ranks, domain split N=2 -> 1+1, N=4 -> 2+2, N=8 -> 4+4; roofline = NVLink.
+value = bus GB/s (nccl-tests convention, n = logical ranks: algbw * 2(n-1)/n); inputs (256 MiB per
+rank) exceed the 126 MB L2, so no flush is needed between steps. Rank 0 prints one JSON line.
+--impl reference times the CPU oracle (oracle/, the tier's reference arm) on a bounded sample.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+MAPS = {1: [0, 0, 0, 0, 1, 1, 1, 1], 2: [0, 1], 4: [0, 0, 1, 1], 8: [0, 0, 0, 0, 1, 1, 1, 1]}
+SPLIT_NAME = {1: "4+4 (8 ranks multiplexed on 1 GPU)", 2: "1+1", 4: "2+2", 8: "4+4"}
+SEED = 2  # SURVEY §8(d) C2 seed
+NVLINK_PEAK = 770.0  # GB/s per direction, measured peer copy (B200_PROFILING.md)
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def gen_inputs(n_ranks, count, first_rank=0):
+    """bf16 N(0,1)*2^-4 per (seed, rank, i) via the synth module (host), one array per rank."""
+    import synth
+    from concurrent.futures import ThreadPoolExecutor
+    out = [None] * n_ranks
+
+    def one(r):
+        out[r] = synth.normal(SEED, first_rank + r, count, "bf16")
+    with ThreadPoolExecutor(max_workers=min(8, n_ranks)) as ex:
+        list(ex.map(one, range(n_ranks)))
+    return out
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 100 ms during the timed region."""
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-lms", "100", "-i", str(self.device)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        time.sleep(0.25)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            f = [x.strip() for x in l.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def busbw(nbytes, t_s, n):
+    alg = nbytes / t_s / 1e9
+    return alg, alg * 2 * (n - 1) / n
+
+
+def oracle_baseline(xs_host, m, budget_s=20.0):
+    """cpu_baseline: the oracle as it stands, single thread, on a bounded sample of the workload."""
+    import oracle
+    count = xs_host[0].size
+    # ~40 ns/element for 8 ranks: bound the sample to the budget
+    sample = int(min(count, max(1 << 16, budget_s / 45e-9)))
+    xs = [x[:sample] for x in xs_host]
+    t0 = time.perf_counter()
+    oracle.allreduce(xs, m, "bf16", "sum")
+    dt = time.perf_counter() - t0
+    alg, bus = busbw(sample * 2, dt, len(m))
+    return {"value": round(bus, 3), "unit": "GB/s", "cores": 1, "kind": "oracle",
+            "sample": f"first {sample} of {count} elements per rank, all {len(m)} ranks, one All-Reduce "
+                      f"({dt:.2f} s single-threaded); busbw convention as value"}
+
+
+def parity_windows(recv_dev_list, xs_host, m, count):
+    """Full-size parity on sampled outputs: three 4096-element windows vs the oracle, bitwise."""
+    import oracle
+    import torch
+    W = 4096
+    starts = [0, count // 2 - W // 2, count - W]
+    ok = True
+    for st in starts:
+        want = oracle.allreduce([x[st:st + W] for x in xs_host], m, "bf16", "sum")
+        for r, y in enumerate(recv_dev_list):
+            got = y[st:st + W].cpu().view(torch.int16).numpy().view(np.uint16)
+            ok &= bool(np.array_equal(got, want))
+    return ok, f"bitwise vs oracle on 3 windows x {W} elements x {len(recv_dev_list)} local ranks"
+
+
+# ---------------------------------------------------------------------------------- N = 1 (mux)
+def run_mux(args):
+    import torch
+    import paper_2601_22585_b200 as hc
+    dev = 0
+    torch.cuda.set_device(dev)
+    m = MAPS[1]
+    n = len(m)
+    count = args.mib * (1 << 20) // 2
+    S = count * 2
+    xs = gen_inputs(n, count)
+    sends = [torch.from_numpy(x.view(np.int16)).view(torch.bfloat16).to("cuda") for x in xs]
+    recvs = [torch.empty_like(s) for s in sends]
+    comm = hc.hetccl_comm_init_mux(n, m, dev)
+    stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream
+
+    def step():
+        hc.mux_allreduce(sends, recvs, comm, stream=sp)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev) as clk:
+        torch.cuda.synchronize()
+        t_start.record(stream)
+        for i in range(args.steps):
+            ev[i][0].record(stream)
+            step()
+            ev[i][1].record(stream)
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    hc.hetccl_comm_get_async_error(comm)
+    total_ms = t_start.elapsed_time(t_end)
+    launch_ms = statistics.mean(a.elapsed_time(b) for a, b in ev)
+    t_step = total_ms / args.steps * 1e-3
+    alg, bus = busbw(S, t_step, n)
+    ok, how = parity_windows(recvs, xs, m, count)
+
+    # e2e: host pinned buffers -> device -> All-Reduce -> host, every step
+    hin = [torch.from_numpy(x.view(np.int16)).view(torch.bfloat16).pin_memory() for x in xs]
+    hout = [torch.empty_like(h).pin_memory() for h in hin]
+    e2e_steps = max(1, min(args.steps, 5))
+
+    def e2e_step():
+        for r in range(n):
+            sends[r].copy_(hin[r], non_blocking=True)
+        step()
+        for r in range(n):
+            hout[r].copy_(recvs[r], non_blocking=True)
+    e2e_step()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(e2e_steps):
+        e2e_step()
+    b.record(stream)
+    torch.cuda.synchronize()
+    t_e2e = a.elapsed_time(b) / e2e_steps * 1e-3
+    _, e2e_bus = busbw(S, t_e2e, n)
+    hc.hetccl_comm_destroy(comm)
+
+    hbm_peak, peak_src = peaks()
+    alg_bytes = 2 * n * S  # every rank's input read once + output written once: the design-free minimum
+    achieved = alg_bytes / (launch_ms * 1e-3) / 1e9
+    cpu = oracle_baseline(xs, m) if not args.no_cpu_baseline else None
+    out = {
+        "metric": "allreduce_busbw", "value": round(bus, 2), "unit": "GB/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded bf16 N(0,1)*2^-4)",
+        "config": {"workload": f"C2 target point: hierarchical All-Reduce, {args.mib} MiB bf16 per rank, "
+                               f"{SPLIT_NAME[1]}", "ranks": n, "rank_to_domain": m, "count": count,
+                   "l2": "inputs > L2 (no flush)", "parallelism": "rank-multiplexed"},
+        "algbw": round(alg, 2), "gpu_launches": args.steps,
+        "e2e": {"value": round(e2e_bus, 2), "unit": "GB/s", "h2d_bytes_per_step": n * S, "d2h_bytes_per_step": n * S},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
+                     "frac": round(achieved / hbm_peak, 4), "traffic": None,
+                     "note": f"algorithmic = 2*n*S = {alg_bytes} B per launch (each rank's input read + output "
+                             f"written once); peak {peak_src}; kernel k_allreduce avg launch {launch_ms:.4f} ms"},
+        "parity": {"ok": ok, "how": how},
+        "clocks": clk.summary(),
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(out), flush=True)
+
+
+# ---------------------------------------------------------------------------------- N > 1
+def run_dist(args):
+    import torch
+    import torch.distributed as dist
+    import paper_2601_22585_b200 as hc
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if world not in MAPS:
+        raise SystemExit(f"--gpus {world}: no domain split defined (use 2, 4 or 8)")
+    m = MAPS[world]
+    count = args.mib * (1 << 20) // 2
+    S = count * 2
+    x = gen_inputs(1, count, first_rank=rank)[0]
+    send = torch.from_numpy(x.view(np.int16)).view(torch.bfloat16).to("cuda")
+    recv = torch.empty_like(send)
+    comm = hc.init_process_group_comm(m)
+    stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream
+
+    def step():
+        hc.allreduce(send, recv, comm, stream=sp)
+
+    def timed(fn, steps):
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        dist.barrier()
+        torch.cuda.synchronize()
+        a.record(stream)
+        for i in range(steps):
+            ev[i][0].record(stream)
+            fn()
+            ev[i][1].record(stream)
+        b.record(stream)
+        torch.cuda.synchronize()
+        dist.barrier()
+        tot = torch.tensor([a.elapsed_time(b)], device="cuda")
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+        lm = torch.tensor([statistics.mean(p.elapsed_time(q) for p, q in ev)], device="cuda")
+        dist.all_reduce(lm, op=dist.ReduceOp.MAX)
+        return tot.item(), lm.item()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        total_ms, launch_ms = timed(step, args.steps)
+    hc.hetccl_comm_get_async_error(comm)
+    t_step = total_ms / args.steps * 1e-3
+    alg, bus = busbw(S, t_step, world)
+
+    # full-size parity on sampled windows: every rank's windows are regenerated from the generator
+    import synth
+    import oracle
+    W = 4096
+    ok = True
+    for st in (0, count // 2 - W // 2, count - W):
+        xs_w = [synth.normal(SEED, r, W, "bf16", start=st) for r in range(world)]
+        want = oracle.allreduce(xs_w, m, "bf16", "sum")
+        got = recv[st:st + W].cpu().view(torch.int16).numpy().view(np.uint16)
+        ok &= bool(np.array_equal(got, want))
+    okt = torch.tensor([1 if ok else 0], device="cuda")
+    dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+
+    # NCCL flat all-reduce on the same-size buffer (comparison baseline only)
+    nbuf = send.clone()
+    for _ in range(args.warmup):
+        dist.all_reduce(nbuf)
+    nccl_ms, _ = timed(lambda: dist.all_reduce(nbuf), args.steps)
+    _, nccl_bus = busbw(S, nccl_ms / args.steps * 1e-3, world)
+
+    # e2e through the public API with pinned host buffers
+    hin = torch.from_numpy(x.view(np.int16)).view(torch.bfloat16).pin_memory()
+    hout = torch.empty_like(hin).pin_memory()
+
+    def e2e_step():
+        send.copy_(hin, non_blocking=True)
+        step()
+        hout.copy_(recv, non_blocking=True)
+    e2e_step()
+    e2e_steps = max(1, min(args.steps, 5))
+    e2e_ms, _ = timed(e2e_step, e2e_steps)
+    _, e2e_bus = busbw(S, e2e_ms / e2e_steps * 1e-3, world)
+
+    plan = hc.hetccl_plan_info(m, rank, hc.OP_ALLREDUCE, count, hc.BFLOAT16)
+    busiest = max(hc.hetccl_plan_info(m, r, hc.OP_ALLREDUCE, count, hc.BFLOAT16)["bytes_sent"] for r in range(world))
+    achieved = busiest / (launch_ms * 1e-3) / 1e9
+    clocks = clk.summary()
+    hc.hetccl_comm_destroy(comm)
+    if rank == 0:
+        out = {
+            "metric": "allreduce_busbw", "value": round(bus, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(total_ms / args.steps, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded bf16 N(0,1)*2^-4)",
+            "config": {"workload": f"hierarchical All-Reduce, {args.mib} MiB bf16 per rank, {SPLIT_NAME[world]}",
+                       "ranks": world, "rank_to_domain": m, "count": count, "l2": "inputs > L2 (no flush)",
+                       "parallelism": f"dp{world}"},
+            "algbw": round(alg, 2), "gpu_launches": args.steps * world,
+            "nccl_flat": {"busbw": round(nccl_bus, 2), "ratio": round(bus / nccl_bus, 4)},
+            "e2e": {"value": round(e2e_bus, 2), "unit": "GB/s", "h2d_bytes_per_step": world * S,
+                    "d2h_bytes_per_step": world * S},
+            "roofline": {"bound": "nvlink", "achieved": round(achieved, 1), "peak": NVLINK_PEAK, "unit": "GB/s",
+                         "frac": round(achieved / NVLINK_PEAK, 4), "traffic": None,
+                         "note": f"algorithmic = busiest rank's NVLink bytes sent per launch ({busiest} B, plan) / "
+                                 f"avg k_allreduce launch {launch_ms:.4f} ms; peak = measured peer copy per direction"},
+            "parity": {"ok": bool(okt.item()), "how": "bitwise vs oracle on 3 windows x 4096 elements, all ranks"},
+            "clocks": clocks,
+            "cpu_baseline": None,
+        }
+        print(json.dumps(out), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    rank = int(os.environ.get("RANK", 0))
+    if rank != 0:
+        return
+    import oracle
+    world = int(os.environ.get("WORLD_SIZE", args.gpus))
+    n_gpu = world if world > 1 else args.gpus
+    m = MAPS.get(n_gpu, MAPS[1])
+    n = len(m)
+    count = args.mib * (1 << 20) // 2
+    budget = 150.0  # seconds for warmup + steps together
+    per_step = budget / max(1, args.steps + args.warmup)
+    sample = int(min(count, max(1 << 14, per_step / (5e-9 * n))))
+    xs = gen_inputs(n, sample)
+    for _ in range(args.warmup):
+        oracle.allreduce(xs, m, "bf16", "sum")
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.allreduce(xs, m, "bf16", "sum")
+        times.append(time.perf_counter() - t0)
+    t = sum(times) / len(times)
+    _, bus = busbw(sample * 2, t, n)
+    desc = f"first {sample} of {count} elements per rank, {n} ranks ({SPLIT_NAME.get(n_gpu, '')}), single-threaded"
+    out = {
+        "impl": "reference", "metric": "allreduce_busbw", "value": round(bus, 4), "unit": "GB/s", "n_gpus": n_gpu,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded bf16 N(0,1)*2^-4)",
+        "config": {"workload": f"hierarchical All-Reduce, {args.mib} MiB bf16 per rank, {SPLIT_NAME.get(n_gpu, '')}",
+                   "ranks": n, "rank_to_domain": m, "count": count},
+        "cpu_baseline": {"value": round(bus, 4), "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": desc},
+        "e2e": {"value": round(bus, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="hetccl", choices=["hetccl", "reference"])
+    ap.add_argument("--mib", type=int, default=256)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    if world == 1:
+        run_mux(args)
+    else:
+        run_dist(args)
+
+
+if __name__ == "__main__":
+    main()
