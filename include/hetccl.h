@@ -173,6 +173,25 @@ typedef struct {
 HETCCL_API hetcclResult_t hetccl_plan_info(int nranks, const int* rank_to_domain, int rank, int op, size_t count,
                                 hetcclDataType_t dt, int root, int nchannels, hetcclPlanInfo_t* info);
 
+/*
+ * Host-only (no CUDA): the pipeline schedule `rank` runs for one op. Logical stage s
+ * (0..nstages-1) is active iff bit s of `active` is set (identical on every rank). Before stage s of
+ * a tile, every sender in wait_mask[s] must have signalled counter wait_ctr[s] (0 S1, 1 S2, 2 AG,
+ * 3 S3; 7 = none) for that tile; after it, counter sig_ctr[s] of every rank in sig_mask[s] is
+ * signalled. `writes` = ranks whose scratch this rank writes. For tests of the protocol's symmetry.
+ */
+typedef struct {
+  int nstages;
+  unsigned int active;
+  int wait_ctr[8];
+  unsigned int wait_mask[8];
+  int sig_ctr[8];
+  unsigned int sig_mask[8];
+  unsigned int writes;
+} hetcclStagePlan_t;
+HETCCL_API hetcclResult_t hetccl_plan_stages(int nranks, const int* rank_to_domain, int rank, int op, int root,
+                                             hetcclStagePlan_t* plan);
+
 #ifdef __cplusplus
 }
 #endif

@@ -30,6 +30,12 @@ class HetcclError(RuntimeError):
         super().__init__(f"{_RESULT.get(code, code)}: {detail}")
 
 
+class StagePlan(ctypes.Structure):
+    _fields_ = [("nstages", ctypes.c_int), ("active", ctypes.c_uint), ("wait_ctr", ctypes.c_int * 8),
+                ("wait_mask", ctypes.c_uint * 8), ("sig_ctr", ctypes.c_int * 8), ("sig_mask", ctypes.c_uint * 8),
+                ("writes", ctypes.c_uint)]
+
+
 class PlanInfo(ctypes.Structure):
     _fields_ = [("bytes_sent", ctypes.c_size_t), ("bytes_recv", ctypes.c_size_t), ("tile_elems", ctypes.c_size_t),
                 ("ntiles", ctypes.c_size_t), ("nchannels", ctypes.c_int), ("nslots", ctypes.c_int)]
@@ -41,6 +47,7 @@ EXPORTED = [
     "hetccl_comm_get_async_error", "hetccl_get_error_string", "hetccl_get_last_error", "hetccl_allreduce",
     "hetccl_reduce_scatter", "hetccl_all_gather", "hetccl_broadcast", "hetccl_mux_allreduce",
     "hetccl_mux_reduce_scatter", "hetccl_mux_all_gather", "hetccl_mux_broadcast", "hetccl_plan_info",
+    "hetccl_plan_stages",
 ]
 
 _lib = None
@@ -76,6 +83,7 @@ def lib():
         "hetccl_mux_all_gather": [pp, pp, c_size, c_int, vp, vp],
         "hetccl_mux_broadcast": [pp, pp, c_size, c_int, c_int, vp, vp],
         "hetccl_plan_info": [c_int, ip, c_int, c_int, c_size, c_int, c_int, c_int, ctypes.POINTER(PlanInfo)],
+        "hetccl_plan_stages": [c_int, ip, c_int, c_int, c_int, ctypes.POINTER(StagePlan)],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -185,6 +193,16 @@ def hetccl_plan_info(rank_to_domain, rank, op, count, dtype=BFLOAT16, root=0, nc
     _check(lib().hetccl_plan_info(len(rank_to_domain), _imap(rank_to_domain), rank, op, count, dtype, root,
                                   nchannels, ctypes.byref(info)))
     return {f: getattr(info, f) for f, _ in PlanInfo._fields_}
+
+
+def hetccl_plan_stages(rank_to_domain, rank, op, root=0):
+    """The pipeline schedule of `rank` for op (host-only): dict of nstages, active, and per logical
+    stage wait_ctr / wait_mask / sig_ctr / sig_mask lists, plus writes."""
+    p = StagePlan()
+    _check(lib().hetccl_plan_stages(len(rank_to_domain), _imap(rank_to_domain), rank, op, root, ctypes.byref(p)))
+    n = p.nstages
+    return {"nstages": n, "active": p.active, "wait_ctr": list(p.wait_ctr)[:n], "wait_mask": list(p.wait_mask)[:n],
+            "sig_ctr": list(p.sig_ctr)[:n], "sig_mask": list(p.sig_mask)[:n], "writes": p.writes}
 
 
 def init_process_group_comm(rank_to_domain, rank=None, world_size=None, device=None, group=None):

@@ -1,31 +1,35 @@
-// hetccl_internal.h — structures shared by the host runtime (plan.cpp, comm.cu, api.cu) and the
-// device kernels (kernels.cu). Not part of the ABI.
+// hetccl_internal.h — structures shared by the host runtime (plan.cpp, runtime.cu) and the device
+// kernels (kernels.cu). Not part of the ABI.
 //
 // Data layout in HBM:
-//   per rank, one cudaMalloc'd, IPC-exported region  = [ flags | scratch ]
-//   flags   : kMaxChannels x kCounters counters, each on its own 128-B line (kFlagStride words)
-//             counters C_S1..C_ACK are written by PEERS (red.release.sys.add) and polled locally
-//             (ld.acquire.sys); line C_BASE holds this rank's own cumulative "expected" values, so
-//             the protocol survives CUDA-graph replay (no host-side sequence numbers).
-//   scratch : kMaxChannels x kNumSlots slots of slot_elems elements; a slot holds every staging
-//             buffer one tile of one op needs on this rank (layout per op in kernels.cu).
+//   per rank, one cudaMalloc'd, IPC-exported region = [ flags | base | scratch ]
+//   flags   : [channel][counter] lines of 128 B; word p of a line counts the signals SENDER p has
+//             delivered to this rank on that (channel, counter). Written only by peers
+//             (red.release... see kernels.cu), polled locally (ld.acquire.sys), one lane per sender.
+//   base    : same shape; this rank's own cumulative "expected so far" per (channel, counter,
+//             sender), advanced by each launch at exit, plus the channel's cumulative tile count in
+//             word 0 of counter line kCounters. Targets are cumulative across launches, so the
+//             protocol needs no host sequence numbers and survives CUDA-graph replay.
+//   scratch : [channel][slot] ring of kNumSlots slots of slot_elems elements; slot g % kNumSlots
+//             holds every staging buffer cumulative tile g of that channel needs on this rank.
 #pragma once
 #include <stddef.h>
 #include <stdint.h>
 
 namespace hetccl {
 
-constexpr int kMaxRanks = 16;     // == HETCCL_MAX_RANKS
-constexpr int kMaxChannels = 64;  // hard cap on CTAs per rank per op
-constexpr int kNumSlots = 2;      // scratch ring depth per channel
-constexpr int kThreads = 512;     // threads per CTA
-constexpr int kFlagStride = 16;   // uint64 words per counter line (128 B)
+constexpr int kMaxRanks = 16;      // == HETCCL_MAX_RANKS (one flag line = 16 senders x 8 B)
+constexpr int kMaxChannels = 148;  // hard cap on CTAs per rank per op (one per SM)
+constexpr int kNumSlots = 8;       // scratch ring depth per channel (> pipeline depth)
+constexpr int kThreads = 512;      // threads per CTA
+constexpr int kMaxStages = 5;      // pipeline positions of the deepest op (All-Reduce)
 
-// counters (per rank, per channel)
-enum : int { C_S1 = 0, C_S2 = 1, C_AG = 2, C_S3 = 3, C_ACK = 4, C_NREMOTE = 5, C_BASE = 5, kCounters = 6 };
-constexpr size_t kChanWords = (size_t)kCounters * kFlagStride;
-constexpr size_t kFlagsBytes = (size_t)kMaxChannels * kChanWords * sizeof(uint64_t);  // 48 KiB
-constexpr size_t kFlagsReserve = 64 * 1024;  // scratch starts here (256-B aligned)
+// counters (per rank, per channel); C_ACK counts tiles a sender has fully consumed
+enum : int { C_S1 = 0, C_S2 = 1, C_AG = 2, C_S3 = 3, C_ACK = 4, kCounters = 5, C_NONE = 7 };
+constexpr size_t kLineWords = 16;  // uint64 words per 128-B line
+constexpr size_t kChanWords = (size_t)(kCounters + 1) * kLineWords;  // + one line of channel state
+constexpr size_t kFlagsBytes = (size_t)kMaxChannels * kChanWords * sizeof(uint64_t);
+constexpr size_t kFlagsReserve = 2 * ((kFlagsBytes + 65535) / 65536) * 65536;  // flags + base, 64K aligned
 
 enum OpKind : int { OP_ALLREDUCE = 0, OP_REDUCE_SCATTER = 1, OP_ALL_GATHER = 2, OP_BROADCAST = 3, OP_COPY = 4 };
 enum DType : int { DT_INT32 = 2, DT_F16 = 6, DT_F32 = 7, DT_BF16 = 9 };
@@ -50,13 +54,23 @@ struct RankMem {
   char* scratch;
 };
 
-// Per-op, per-rank protocol constants computed by the host plan.
+// Per-op, per-rank schedule computed by the host plan (plan.cpp). Pipeline position s of an op is
+// the same on every rank; a stage with no work on this rank still holds its position.
+//   wait_ctr[s] / wait_mask[s]: before stage s of tile t, every sender in wait_mask must have
+//                               signalled counter wait_ctr[s] for tile t;
+//   sig_ctr[s]  / sig_mask[s] : after stage s of tile t, signal counter sig_ctr[s] of every rank in
+//                               sig_mask (exactly once per tile).
+// Consistency (checked by tests): r in sig_mask_w[s] on counter c <=> w in wait_mask_r[s'] where
+// wait_ctr_r[s'] == c, with s < s' (a producer always precedes its consumer in the pipeline).
 struct RankPlan {
-  uint32_t partners;      // bitmask of ranks this rank exchanges data with (symmetric)
-  uint32_t inc[C_NREMOTE];  // arrivals per tile on each counter (C_ACK: acks per tile)
+  uint8_t wait_ctr[kMaxStages];
+  uint8_t sig_ctr[kMaxStages];
+  uint16_t wait_mask[kMaxStages];
+  uint16_t sig_mask[kMaxStages];
+  uint16_t writes;  // ranks whose scratch this rank writes (ACK wait before reusing a slot)
 };
 
-// Kernel parameters (passed by value as a __grid_constant__; < 4 KiB).
+// Kernel parameters (passed by value as a __grid_constant__).
 struct OpArgs {
   Topo topo;
   RankMem mem[kMaxRanks];
@@ -69,6 +83,7 @@ struct OpArgs {
   size_t ntiles;
   size_t slot_elems;            // elements per scratch slot
   int nch;
+  uint32_t active;              // bitmask of the op's logical stages that are active (same on all ranks)
   int root;
   int op;
   unsigned long long* err;      // device error word of the comm
@@ -81,9 +96,10 @@ struct Geometry {
   size_t tile, ntiles;
   int nch;
 };
-// q = alignment quantum of a tile in elements
 Geometry make_geometry(const Topo& t, int op, size_t count, int es, int nch_max, size_t slot_elems);
 size_t slot_mult_num(const Topo& t, int op, size_t tile);  // scratch elements one slot needs for `tile`
+int op_stages(int op);                                      // logical stages of op
+uint32_t active_stages(const Topo& t, int op, int root);   // active logical stages (same on all ranks)
 void make_rank_plan(const Topo& t, int op, int rank, int root, RankPlan* rp);
 void plan_bytes(const Topo& t, int op, int rank, int root, size_t count, int es, size_t tile, size_t* sent,
                 size_t* recv);

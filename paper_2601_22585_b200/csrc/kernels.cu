@@ -1,18 +1,22 @@
 // kernels.cu — sm_100a device code of the hierarchical collectives.
 //
-// One persistent CTA per (channel, local rank). A channel walks the tiles t = ch, ch+nch, ... of the
-// op; every stage of a tile moves data with 16-byte vector loads/stores — remote stores go straight
-// into a peer's IPC-mapped scratch slot over NVLink 5 / NVSwitch ("push"), all reads are local —
-// and hands off to the next stage through per-(rank, channel, stage) counters:
+// One persistent CTA per (channel, local rank). Every op is a short list of stages (All-Reduce:
+// A intra push, B intra fold + cross push, C cross fold + AG push, D final region -> y and domain
+// peers, E peers' regions -> y); a channel runs them as a SOFTWARE PIPELINE over its tiles
+// t = ch, ch+nch, ...: iteration i runs stage at position p on the channel's tile i-p, so the
+// intra-domain and cross-domain stages of different tiles overlap and no flag round trip sits on
+// the critical path (run_pipeline). Data moves with 16-byte vector loads/stores; remote stores go
+// straight into a peer's IPC-mapped scratch slot over NVLink 5 / NVSwitch ("push"), all loads are
+// local. Hand-off between stages uses per-(receiver, channel, counter, SENDER) counters:
 //   writer: data stores -> __syncthreads -> fence.acq_rel.sys -> red.relaxed.sys.add(+1) on the
-//           receiver's counter;
-//   reader: thread 0 spins ld.acquire.sys until the counter reaches its cumulative target ->
-//           __syncthreads -> ld.global.cg of the staged data.
-// Slots are a ring of kNumSlots per channel; before writing tile t a rank waits until every
-// receiver has acked tile t - kNumSlots (C_ACK). Targets are cumulative across launches (bases kept
-// in the rank's own flag line C_BASE), so the protocol needs no host sequence numbers and replays
-// under CUDA graphs. The same kernels serve the rank-multiplexed mode (all ranks on one device,
-// rank = blockIdx.y, cooperative launch) and the one-rank-per-GPU mode (gridDim.y = 1).
+//           receiver's counter word of this sender;
+//   reader: lane p of warp 0 spins ld.acquire.sys on sender p's word until it reaches the
+//           cumulative target -> __syncthreads -> ld.global.cg of the staged data.
+// Scratch is a ring of kNumSlots slots per channel indexed by the channel's cumulative tile count;
+// before writing a tile's slot a rank waits for the ACK of the tile that last used it. Targets are
+// cumulative across launches (kept in the rank's own base lines), so the protocol needs no host
+// sequence numbers and replays under CUDA graphs. The same kernels serve the rank-multiplexed mode
+// (all ranks on one device, rank = blockIdx.y, cooperative launch) and the one-rank-per-GPU mode.
 //
 // Arithmetic (readings R3, R5, R6, R8): per element, fold ascending rank inside a domain
 // (seeded with the first operand), narrow 16-bit types once at the domain boundary (stored partial),
@@ -164,11 +168,12 @@ __device__ __forceinline__ bool all_aligned16(const PtrList& a, const PtrList& b
   return (o & 15) == 0;
 }
 
-constexpr int kUnroll = 4;
+constexpr int kUnroll = 4;      // vectors in flight per thread per source in a fold
+constexpr int kCopyUnroll = 8;  // vectors in flight per thread in a copy
 
 // dst[d][i] = src[i] for every destination d, i < n elements of size ES (bit copy)
 template <int ES>
-__device__ void cta_copy(const void* src, const PtrList& dsts, size_t n) {
+__device__ __noinline__ void cta_copy(const void* src, const PtrList& dsts, size_t n) {
   if (n == 0) return;
   constexpr int V = 16 / ES;
   const int tid = threadIdx.x, nth = blockDim.x;
@@ -176,17 +181,17 @@ __device__ void cta_copy(const void* src, const PtrList& dsts, size_t n) {
   s1.add(src);
   const size_t nv = all_aligned16(s1, dsts) ? n / V : 0;
   const char* sp = (const char*)src;
-  for (size_t v0 = tid; v0 < nv; v0 += (size_t)kUnroll * nth) {
-    uint4 w[kUnroll];
+  for (size_t v0 = tid; v0 < nv; v0 += (size_t)kCopyUnroll * nth) {
+    uint4 w[kCopyUnroll];
 #pragma unroll
-    for (int u = 0; u < kUnroll; u++) {
+    for (int u = 0; u < kCopyUnroll; u++) {
       size_t v = v0 + (size_t)u * nth;
       if (v < nv) w[u] = ld_v4(sp + v * 16);
     }
     for (int d = 0; d < dsts.n; d++) {
       char* dp = (char*)dsts.p[d];
 #pragma unroll
-      for (int u = 0; u < kUnroll; u++) {
+      for (int u = 0; u < kCopyUnroll; u++) {
         size_t v = v0 + (size_t)u * nth;
         if (v < nv) st_v4(dp + v * 16, w[u]);
       }
@@ -212,7 +217,7 @@ __device__ __forceinline__ void cta_copy1(const void* src, void* dst, size_t n) 
 
 // dst[d][i] = narrow( fold_{s in order} widen(src[s][i]) ) for every destination d
 template <typename T, int OP>
-__device__ void cta_fold(const PtrList& srcs, const PtrList& dsts, size_t n) {
+__device__ __noinline__ void cta_fold(const PtrList& srcs, const PtrList& dsts, size_t n) {
   using TR = Tr<T>;
   using S = typename TR::S;
   using A = typename TR::A;
@@ -286,78 +291,18 @@ __device__ void cta_fold(const PtrList& srcs, const PtrList& dsts, size_t n) {
 __device__ __forceinline__ uint64_t* chan_flags(const OpArgs& a, int rank, int ch) {
   return a.mem[rank].flags + (size_t)ch * kChanWords;
 }
+__device__ __forceinline__ uint64_t* chan_base(const OpArgs& a, int rank, int ch) {
+  return (uint64_t*)((char*)a.mem[rank].flags + kFlagsReserve / 2) + (size_t)ch * kChanWords;
+}
 
 template <typename T>
 __device__ __forceinline__ T* slot_ptr(const OpArgs& a, int rank, int ch, int slot) {
   return (T*)(a.mem[rank].scratch + ((size_t)(ch * kNumSlots + slot) * a.slot_elems) * sizeof(T));
 }
 
-struct CtaState {
-  unsigned long long base[C_NREMOTE];
-  int abort_;
-};
-
-__device__ __forceinline__ void cta_begin(CtaState& st, const uint64_t* F) {
-  if (threadIdx.x == 0) {
-    for (int c = 0; c < C_NREMOTE; c++) st.base[c] = F[C_BASE * kFlagStride + c];
-    st.abort_ = 0;
-  }
-  __syncthreads();
-}
-
-// all threads: completes every data store of this CTA, then adds cnt[r] to counter `ctr` of
-// channel `ch` on every rank r with cnt[r] > 0 (lane r of warp 0 signals rank r)
-__device__ __forceinline__ void cta_signal(const OpArgs& a, int ch, int ctr, const uint32_t* cnt) {
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    fence_acq_rel_sys();
-    const int r = threadIdx.x;
-    if (r < a.topo.n && cnt[r]) red_add_relaxed_sys(chan_flags(a, r, ch) + ctr * kFlagStride, cnt[r]);
-  }
-}
-
-__device__ __forceinline__ void cta_signal_mask(const OpArgs& a, int ch, int ctr, uint32_t mask) {
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    fence_acq_rel_sys();
-    const int r = threadIdx.x;
-    if ((mask >> r) & 1u) red_add_relaxed_sys(chan_flags(a, r, ch) + ctr * kFlagStride, 1);
-  }
-}
-
-// all threads: wait until my counter `ctr` >= target (thread 0 polls); false on timeout
-__device__ __noinline__ bool cta_wait(const OpArgs& a, CtaState& st, const uint64_t* F, int ctr, uint64_t target) {
-  if (threadIdx.x == 0) {
-    const uint64_t* p = F + ctr * kFlagStride;
-    if (ld_acquire_sys(p) < target) {
-      const uint64_t t0 = globaltimer();
-      uint32_t it = 0;
-      while (ld_acquire_sys(p) < target) {
-        if ((++it & 1023u) == 0 && (long long)(globaltimer() - t0) > a.timeout_ns) {
-          atomicOr(a.err, 1ull + ((unsigned long long)ctr << 8));
-          *(volatile int*)&st.abort_ = 1;
-          break;
-        }
-      }
-    }
-  }
-  __syncthreads();
-  return *(volatile int*)&st.abort_ == 0;
-}
-
-__device__ __forceinline__ void cta_end(CtaState& st, uint64_t* F, const RankPlan& rp, int tiles_done) {
-  __syncthreads();
-  if (threadIdx.x == 0 && st.abort_ == 0)
-    for (int c = 0; c < C_NREMOTE; c++) F[C_BASE * kFlagStride + c] = st.base[c] + (uint64_t)tiles_done * rp.inc[c];
-}
-
-__device__ __forceinline__ uint64_t ack_target(const CtaState& st, const RankPlan& rp, int tl) {
-  return st.base[C_ACK] + (uint64_t)(tl >= kNumSlots ? tl - kNumSlots + 1 : 0) * rp.inc[C_ACK];
-}
-
 __device__ __forceinline__ size_t floor_to(size_t x, size_t q) { return x / q * q; }
 
-// elementary-segment and piece boundaries of one tile (same formulas as plan.cpp)
+// elementary-segment and piece boundaries of one AR tile (same formulas as plan.cpp)
 struct Geo {
   size_t len;
   int L, D, V;
@@ -377,166 +322,279 @@ __device__ __forceinline__ int owner_of(const Topo& t, int q, int s) {
   return t.members[t.dom_first[q] + s / (t.L / t.dom_size[q])];
 }
 
+// ================================================================== pipeline driver ===========
+// Software pipeline over the tiles t = ch, ch + nch, ... of one channel. The op's active logical
+// stages occupy positions 0..np-1 (identical on every rank); iteration `it` runs the stage at
+// position p on the channel's local tile it - p. Per iteration:
+//   1. warp 0, lane p polls sender p's counters: for every stage due this iteration, its wait
+//      counter must show the tile (cumulative target base + tile + 1); position 0 also waits for
+//      the ACK of the tile that last used the slot (slot reuse, kNumSlots deep ring);
+//   2. __syncthreads; every stage due runs on its tile (all 512 threads, 16-byte vectors);
+//   3. __syncthreads; warp 0 executes fence.acq_rel.sys (all data of the iteration, local and
+//      remote, is performed at system scope), then lane r adds 1 to rank r's counter for every
+//      stage that signals r; after the last position's tile, every other rank gets an ACK.
+// A producer stage always sits at an earlier position than its consumer and kNumSlots exceeds the
+// pipeline depth, so every wait of iteration it depends only on iterations < it of other ranks:
+// no cycle, hence no deadlock with all CTAs co-resident.
+struct PipeShared {
+  unsigned long long base[kCounters][kMaxRanks];
+  unsigned long long tiles0;
+  int abort_;
+};
+
+template <class Op>
+__device__ __forceinline__ void run_pipeline(const OpArgs& a, Op& op, int me, int ch) {
+  __shared__ PipeShared ps;
+  const RankPlan& rp = a.rp[me];
+  const int n = a.topo.n;
+  uint64_t* F = chan_flags(a, me, ch);
+  uint64_t* B = chan_base(a, me, ch);
+  int stage_at[kMaxStages];
+  int np = 0;
+#pragma unroll
+  for (int s = 0; s < kMaxStages; s++)
+    if ((a.active >> s) & 1u) stage_at[np++] = s;
+  if (threadIdx.x < kCounters * kMaxRanks) ps.base[threadIdx.x / kMaxRanks][threadIdx.x % kMaxRanks] = B[threadIdx.x / kMaxRanks * kLineWords + threadIdx.x % kMaxRanks];
+  if (threadIdx.x == 0) {
+    ps.tiles0 = B[kCounters * kLineWords];
+    ps.abort_ = 0;
+  }
+  __syncthreads();
+  const long long ntl = (ch < (long long)a.ntiles) ? ((long long)a.ntiles - ch + a.nch - 1) / a.nch : 0;
+  const unsigned long long tiles0 = ps.tiles0;
+  const int lane = threadIdx.x & 31;
+  for (long long it = 0; it < ntl + np - 1; ++it) {
+    // ---- 1. waits (warp 0; lane = sender) ----
+    if (threadIdx.x < 32) {
+      bool ok = true;
+      if (lane < n) {
+        for (int p = 0; p < np && ok; p++) {
+          const long long tl = it - p;
+          if (tl < 0 || tl >= ntl) continue;
+          const int s = stage_at[p];
+          const uint64_t* w1 = nullptr;
+          uint64_t t1 = 0;
+          if (p == 0 && ((rp.writes >> lane) & 1u) && tiles0 + tl >= (unsigned long long)kNumSlots) {
+            w1 = F + C_ACK * kLineWords + lane;
+            t1 = tiles0 + tl - kNumSlots + 1;
+          }
+          const int wc = rp.wait_ctr[s];
+          const uint64_t* w2 = nullptr;
+          uint64_t t2 = 0;
+          if (wc != C_NONE && ((rp.wait_mask[s] >> lane) & 1u)) {
+            w2 = F + wc * kLineWords + lane;
+            t2 = ps.base[wc][lane] + tl + 1;
+          }
+          for (int q = 0; q < 2 && ok; q++) {
+            const uint64_t* w = q ? w2 : w1;
+            const uint64_t tg = q ? t2 : t1;
+            if (!w || ld_acquire_sys(w) >= tg) continue;
+            const uint64_t t0 = globaltimer();
+            uint32_t spins = 0;
+            while (ld_acquire_sys(w) < tg) {
+              if ((++spins & 1023u) == 0 && (long long)(globaltimer() - t0) > a.timeout_ns) {
+                atomicOr(a.err, 1ull + ((unsigned long long)(q ? wc : C_ACK) << 8) + ((unsigned long long)lane << 16));
+                ok = false;
+                break;
+              }
+            }
+          }
+        }
+      }
+      if (!ok) ps.abort_ = 1;
+    }
+    __syncthreads();
+    if (*(volatile int*)&ps.abort_) break;
+    // ---- 2. stage work ----
+    for (int p = 0; p < np; p++) {
+      const long long tl = it - p;
+      if (tl < 0 || tl >= ntl) continue;
+      op.stage(stage_at[p], (size_t)ch + (size_t)tl * a.nch, (int)((tiles0 + tl) % kNumSlots));
+    }
+    __syncthreads();
+    // ---- 3. release: fence, then signals ----
+    if (threadIdx.x < 32) {
+      fence_acq_rel_sys();
+      if (lane < n && lane != me) {
+        for (int p = 0; p < np; p++) {
+          const long long tl = it - p;
+          if (tl < 0 || tl >= ntl) continue;
+          const int s = stage_at[p];
+          if (rp.sig_ctr[s] != C_NONE && ((rp.sig_mask[s] >> lane) & 1u))
+            red_add_relaxed_sys(chan_flags(a, lane, ch) + rp.sig_ctr[s] * kLineWords + me, 1);
+        }
+        const long long tl = it - (np - 1);
+        if (tl >= 0 && tl < ntl) red_add_relaxed_sys(chan_flags(a, lane, ch) + C_ACK * kLineWords + me, 1);
+      }
+    }
+  }
+  __syncthreads();
+  // ---- exit: advance this rank's cumulative targets by the tiles this launch processed ----
+  if (!ps.abort_ && threadIdx.x < kMaxRanks) {
+    const int p = threadIdx.x;
+    for (int s = 0; s < kMaxStages; s++) {
+      if (!((a.active >> s) & 1u)) continue;
+      const int wc = rp.wait_ctr[s];
+      if (wc != C_NONE && ((rp.wait_mask[s] >> p) & 1u)) B[wc * kLineWords + p] = ps.base[wc][p] + ntl;
+    }
+    if (p == 0) B[kCounters * kLineWords] = tiles0 + ntl;
+  }
+}
+
 // ================================================================== All-Reduce (a1-a5) =========
 // Slot layout on a rank of domain k (d = d_k, Rk = tile/d):
 //   s1[d][Rk] | s2[D][Rk] | ag[Rk] | s3[d][Rk]
+// Stages: 0 A intra push | 1 B intra fold + cross push | 2 C cross fold + AG push |
+//         3 D final region -> y and domain peers | 4 E domain peers' regions -> y
 template <typename T, int OP>
-__global__ void __launch_bounds__(kThreads, 1) k_allreduce(const __grid_constant__ OpArgs a) {
-  constexpr int ES = sizeof(T);
-  constexpr int V = Tr<T>::V;
-  __shared__ CtaState st;
-  const int row = blockIdx.y, ch = blockIdx.x;
-  const int me = a.local_rank[row];
-  const Topo& tp = a.topo;
-  const int k = tp.rank_dom[me], j = tp.rank_idx[me], d = tp.dom_size[k], D = tp.D, L = tp.L;
-  const int spj = L / d, s_lo = j * spj, s_hi = s_lo + spj;
-  const size_t TL = a.tile, Rk = TL / d;
-  const T* x = (const T*)a.send[row];
-  T* y = (T*)a.recv[row];
-  uint64_t* F = chan_flags(a, me, ch);
-  const RankPlan& rp = a.rp[me];
-  uint32_t dpeers = 0;
-  for (int i = 0; i < d; i++)
-    if (i != j) dpeers |= 1u << tp.members[tp.dom_first[k] + i];
-  cta_begin(st, F);
-  int tl = 0;
-  for (size_t t = ch; t < a.ntiles; t += a.nch, ++tl) {
+struct ArOp {
+  static constexpr int ES = sizeof(T);
+  static constexpr int V = Tr<T>::V;
+  const OpArgs& a;
+  const Topo& tp;
+  int me, ch, k, j, d, D, L, spj, s_lo, s_hi;
+  size_t TL, Rk;
+  const T* x;
+  T* y;
+  __device__ ArOp(const OpArgs& a_, int row, int ch_) : a(a_), tp(a_.topo), ch(ch_) {
+    me = a.local_rank[row];
+    k = tp.rank_dom[me];
+    j = tp.rank_idx[me];
+    d = tp.dom_size[k];
+    D = tp.D;
+    L = tp.L;
+    spj = L / d;
+    s_lo = j * spj;
+    s_hi = s_lo + spj;
+    TL = a.tile;
+    Rk = TL / d;
+    x = (const T*)a.send[row];
+    y = (T*)a.recv[row];
+  }
+  __device__ int peer(int i) const { return tp.members[tp.dom_first[k] + i]; }
+  // start of the region of owner o (domain q) within a tile, and o's Rk
+  __device__ size_t region_lo(const Geo& g, int o) const {
+    const int q = tp.rank_dom[o];
+    return g.seg(tp.rank_idx[o] * (L / tp.dom_size[q]));
+  }
+  __device__ void stage(int s, size_t t, int slot) {
     const size_t tb = t * TL, len = min(TL, a.count - tb);
     const Geo g{len, L, D, V};
-    const int slot = tl % kNumSlots;
-    if (!cta_wait(a, st, F, C_ACK, ack_target(st, rp, tl))) break;
     const size_t r0 = g.seg(s_lo), r1 = g.seg(s_hi);
     T* mine = slot_ptr<T>(a, me, ch, slot);
     T* my_ag = mine + TL + (size_t)D * Rk;
-    // ---- a1: intra-domain reduce-scatter, push my slices to their owners' s1[j] ----
-    if (d > 1) {
+    T* my_s3 = my_ag + Rk;
+    if (s == 0) {  // ---- A: push my data for each domain peer's region to its s1[j] ----
       for (int i = 0; i < d; i++) {
         if (i == j) continue;
-        const int peer = tp.members[tp.dom_first[k] + i];
         const size_t p0 = g.seg(i * spj), p1 = g.seg((i + 1) * spj);
-        cta_copy1<ES>(x + tb + p0, slot_ptr<T>(a, peer, ch, slot) + (size_t)j * Rk, p1 - p0);
+        cta_copy1<ES>(x + tb + p0, slot_ptr<T>(a, peer(i), ch, slot) + (size_t)j * Rk, p1 - p0);
       }
-      cta_signal_mask(a, ch, C_S1, dpeers);
-      if (!cta_wait(a, st, F, C_S1, st.base[C_S1] + (uint64_t)(tl + 1) * rp.inc[C_S1])) break;
-    }
-    // ---- fold my region over the domain (ascending rank); route each piece to its reducer ----
-    for (int s = s_lo; s < s_hi; s++) {
-      for (int q = 0; q < D; q++) {
-        const size_t c0 = g.piece(s, q), c1 = g.piece(s, q + 1);
-        if (c1 <= c0) continue;
-        PtrList src, dst;
-        for (int i = 0; i < d; i++)
-          src.add(i == j ? (const void*)(x + tb + c0) : (const void*)(mine + (size_t)i * Rk + (c0 - r0)));
-        if (D == 1) {
-          dst.add(y + tb + c0);
-          if (d > 1) dst.add(my_ag + (c0 - r0));
-        } else if (q == k) {
-          dst.add(mine + TL + (size_t)k * Rk + (c0 - r0));
-        } else {
-          const int o = owner_of(tp, q, s);
-          const int dq = tp.dom_size[q];
-          const size_t ro = g.seg(tp.rank_idx[o] * (L / dq));
-          dst.add(slot_ptr<T>(a, o, ch, slot) + TL + (size_t)k * (TL / dq) + (c0 - ro));
+    } else if (s == 1) {  // ---- B: fold my region over the domain; route each piece to its reducer ----
+      for (int sg = s_lo; sg < s_hi; sg++) {
+        for (int q = 0; q < D; q++) {
+          const size_t c0 = g.piece(sg, q), c1 = g.piece(sg, q + 1);
+          if (c1 <= c0) continue;
+          PtrList src, dst;
+          for (int i = 0; i < d; i++)
+            src.add(i == j ? (const void*)(x + tb + c0) : (const void*)(mine + (size_t)i * Rk + (c0 - r0)));
+          if (D == 1) {
+            dst.add(y + tb + c0);
+          } else if (q == k) {
+            dst.add(mine + TL + (size_t)k * Rk + (c0 - r0));
+          } else {
+            const int o = owner_of(tp, q, sg);
+            dst.add(slot_ptr<T>(a, o, ch, slot) + TL + (size_t)k * (TL / tp.dom_size[q]) + (c0 - region_lo(g, o)));
+          }
+          cta_fold<T, OP>(src, dst, c1 - c0);
         }
-        cta_fold<T, OP>(src, dst, c1 - c0);
       }
-    }
-    // ---- a2: cross-domain reduce-scatter + all-gather of the partials among segment owners ----
-    if (D > 1) {
-      __shared__ uint32_t cnt[kMaxRanks];
-      if (threadIdx.x < kMaxRanks) {
-        int c = 0;
-        for (int s = s_lo; s < s_hi; s++)
-          for (int q = 0; q < D; q++)
-            if (q != k && owner_of(tp, q, s) == (int)threadIdx.x) c++;
-        cnt[threadIdx.x] = (uint32_t)c;
-      }
-      cta_signal(a, ch, C_S2, cnt);
-      if (!cta_wait(a, st, F, C_S2, st.base[C_S2] + (uint64_t)(tl + 1) * rp.inc[C_S2])) break;
-      for (int s = s_lo; s < s_hi; s++) {
-        const size_t c0 = g.piece(s, k), c1 = g.piece(s, k + 1);
+    } else if (s == 2) {  // ---- C: fold the D partials of my pieces; final piece -> y and other owners ----
+      for (int sg = s_lo; sg < s_hi; sg++) {
+        const size_t c0 = g.piece(sg, k), c1 = g.piece(sg, k + 1);
         if (c1 <= c0) continue;
         PtrList src, dst;
         for (int q = 0; q < D; q++) src.add(mine + TL + (size_t)q * Rk + (c0 - r0));
         dst.add(y + tb + c0);
-        dst.add(my_ag + (c0 - r0));
         for (int q = 0; q < D; q++) {
           if (q == k) continue;
-          const int o = owner_of(tp, q, s);
+          const int o = owner_of(tp, q, sg);
           const int dq = tp.dom_size[q];
-          const size_t ro = g.seg(tp.rank_idx[o] * (L / dq));
-          dst.add(slot_ptr<T>(a, o, ch, slot) + TL + (size_t)D * (TL / dq) + (c0 - ro));
+          dst.add(slot_ptr<T>(a, o, ch, slot) + TL + (size_t)D * (TL / dq) + (c0 - region_lo(g, o)));
         }
         cta_fold<T, OP>(src, dst, c1 - c0);
       }
-      cta_signal(a, ch, C_AG, cnt);
-      if (!cta_wait(a, st, F, C_AG, st.base[C_AG] + (uint64_t)(tl + 1) * rp.inc[C_AG])) break;
-    }
-    // ---- a3: intra-domain all-gather of the final region ----
-    if (d > 1) {
-      PtrList dst;
-      if (D > 1) dst.add(y + tb + r0);
-      for (int i = 0; i < d; i++) {
-        if (i == j) continue;
-        const int peer = tp.members[tp.dom_first[k] + i];
-        dst.add(slot_ptr<T>(a, peer, ch, slot) + TL + (size_t)(D + 1) * Rk + (size_t)j * Rk);
+    } else if (s == 3) {  // ---- D: my final region -> y (pieces from other owners) and to domain peers ----
+      PtrList peers_s3;
+      for (int i = 0; i < d; i++)
+        if (i != j) peers_s3.add(slot_ptr<T>(a, peer(i), ch, slot) + TL + (size_t)(D + 1) * Rk + (size_t)j * Rk);
+      if (D == 1) {
+        cta_copy<ES>(y + tb + r0, peers_s3, r1 - r0);
+      } else {
+        for (int sg = s_lo; sg < s_hi; sg++) {
+          for (int q = 0; q < D; q++) {
+            const size_t c0 = g.piece(sg, q), c1 = g.piece(sg, q + 1);
+            if (c1 <= c0) continue;
+            PtrList dst;
+            for (int i = 0; i < peers_s3.n; i++) dst.add((const char*)peers_s3.p[i] + (c0 - r0) * ES);
+            if (q == k) {
+              if (dst.n) cta_copy<ES>(y + tb + c0, dst, c1 - c0);
+            } else {
+              dst.add(y + tb + c0);
+              cta_copy<ES>(my_ag + (c0 - r0), dst, c1 - c0);
+            }
+          }
+        }
       }
-      cta_copy<ES>(my_ag, dst, r1 - r0);
-      cta_signal_mask(a, ch, C_S3, dpeers);
-      if (!cta_wait(a, st, F, C_S3, st.base[C_S3] + (uint64_t)(tl + 1) * rp.inc[C_S3])) break;
+    } else {  // ---- E: domain peers' final regions -> y ----
       for (int i = 0; i < d; i++) {
         if (i == j) continue;
         const size_t p0 = g.seg(i * spj), p1 = g.seg((i + 1) * spj);
-        cta_copy1<ES>(mine + TL + (size_t)(D + 1) * Rk + (size_t)i * Rk, y + tb + p0, p1 - p0);
+        cta_copy1<ES>(my_s3 + (size_t)i * Rk, y + tb + p0, p1 - p0);
       }
-    } else if (D > 1) {
-      cta_copy1<ES>(my_ag, y + tb + r0, r1 - r0);
     }
-    // ---- tile done: every slot my senders wrote is consumed ----
-    cta_signal_mask(a, ch, C_ACK, rp.partners);
   }
-  cta_end(st, F, rp, tl);
-}
+};
 
 // ================================================================== Reduce-Scatter (a6) ========
 // Per tile (per-shard offsets [tb, tb+len)), member j of domain k owns: its own shard, plus piece j
 // (of d) of every other-domain shard. Slot layout on a rank of domain k (RG = T + (n-d)*T/d):
-//   s1[d][RG] | s2[D][T]    (s1 region: own-shard part at 0, other-domain shard ro at T + ro*T/d)
+//   s1[d][RG] | s2[D][T]    (s1[i]: own-shard part at 0, other-domain shard #ro at T + ro*T/d)
+// Stages: 0 A intra push | 1 B domain fold + cross push | 2 C cross fold -> y
 template <typename T, int OP>
-__global__ void __launch_bounds__(kThreads, 1) k_reduce_scatter(const __grid_constant__ OpArgs a) {
-  constexpr int ES = sizeof(T);
-  constexpr int V = Tr<T>::V;
-  __shared__ CtaState st;
-  const int row = blockIdx.y, ch = blockIdx.x;
-  const int me = a.local_rank[row];
-  const Topo& tp = a.topo;
-  const int n = tp.n, k = tp.rank_dom[me], j = tp.rank_idx[me], d = tp.dom_size[k], D = tp.D;
-  const size_t TL = a.tile, R = a.count, Pc = TL / d, RG = TL + (size_t)(n - d) * Pc;
-  const T* x = (const T*)a.send[row];
-  T* y = (T*)a.recv[row];
-  uint64_t* F = chan_flags(a, me, ch);
-  const RankPlan& rp = a.rp[me];
-  uint32_t dpeers = 0, others = 0;
-  for (int r = 0; r < n; r++) {
-    if (r == me) continue;
-    if (tp.rank_dom[r] == k) dpeers |= 1u << r;
-    else others |= 1u << r;
+struct RsOp {
+  static constexpr int ES = sizeof(T);
+  static constexpr int V = Tr<T>::V;
+  const OpArgs& a;
+  const Topo& tp;
+  int me, ch, n, k, j, d, D;
+  size_t TL, R, Pc, RG;
+  const T* x;
+  T* y;
+  __device__ RsOp(const OpArgs& a_, int row, int ch_) : a(a_), tp(a_.topo), ch(ch_) {
+    me = a.local_rank[row];
+    n = tp.n;
+    k = tp.rank_dom[me];
+    j = tp.rank_idx[me];
+    d = tp.dom_size[k];
+    D = tp.D;
+    TL = a.tile;
+    R = a.count;
+    Pc = TL / d;
+    RG = TL + (size_t)(n - d) * Pc;
+    x = (const T*)a.send[row];
+    y = (T*)a.recv[row];
   }
-  cta_begin(st, F);
-  int tl = 0;
-  for (size_t t = ch; t < a.ntiles; t += a.nch, ++tl) {
+  __device__ void stage(int s, size_t t, int slot) {
     const size_t tb = t * TL, len = min(TL, R - tb);
-    const int slot = tl % kNumSlots;
-    if (!cta_wait(a, st, F, C_ACK, ack_target(st, rp, tl))) break;
     T* mine = slot_ptr<T>(a, me, ch, slot);
     const size_t pj0 = sub_lo(len, d, j, V), pj1 = sub_lo(len, d, j + 1, V);
-    // ---- intra-domain reduce-scatter: send each peer the data of its region ----
-    if (d > 1) {
+    if (s == 0) {  // ---- A: each domain peer gets my data for its region ----
       for (int i = 0; i < d; i++) {
         if (i == j) continue;
-        const int peer = tp.members[tp.dom_first[k] + i];
-        T* dst = slot_ptr<T>(a, peer, ch, slot) + (size_t)j * RG;
-        cta_copy1<ES>(x + (size_t)peer * R + tb, dst, len);
+        const int pr = tp.members[tp.dom_first[k] + i];
+        T* dst = slot_ptr<T>(a, pr, ch, slot) + (size_t)j * RG;
+        cta_copy1<ES>(x + (size_t)pr * R + tb, dst, len);
         const size_t pi0 = sub_lo(len, d, i, V), pi1 = sub_lo(len, d, i + 1, V);
         int ro = 0;
         for (int r = 0; r < n; r++) {
@@ -545,19 +603,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_reduce_scatter(const __grid_con
           ro++;
         }
       }
-      cta_signal_mask(a, ch, C_S1, dpeers);
-      if (!cta_wait(a, st, F, C_S1, st.base[C_S1] + (uint64_t)(tl + 1) * rp.inc[C_S1])) break;
-    }
-    // ---- fold: own shard -> my domain partial; my pieces of other shards -> their owners' s2[k] ----
-    {
-      PtrList src, dst;
-      for (int i = 0; i < d; i++)
-        src.add(i == j ? (const void*)(x + (size_t)me * R + tb) : (const void*)(mine + (size_t)i * RG));
-      if (D == 1) dst.add(y + tb);
-      else dst.add(mine + (size_t)d * RG + (size_t)k * TL);
-      cta_fold<T, OP>(src, dst, len);
-    }
-    if (D > 1) {
+    } else if (s == 1) {  // ---- B: own shard -> domain partial; my pieces of other shards -> their owners ----
+      {
+        PtrList src, dst;
+        for (int i = 0; i < d; i++)
+          src.add(i == j ? (const void*)(x + (size_t)me * R + tb) : (const void*)(mine + (size_t)i * RG));
+        if (D == 1) dst.add(y + tb);
+        else dst.add(mine + (size_t)d * RG + (size_t)k * TL);
+        cta_fold<T, OP>(src, dst, len);
+      }
       int ro = 0;
       for (int r = 0; r < n; r++) {
         if (tp.rank_dom[r] == k) continue;
@@ -571,55 +625,52 @@ __global__ void __launch_bounds__(kThreads, 1) k_reduce_scatter(const __grid_con
         cta_fold<T, OP>(src, dst, pj1 - pj0);
         ro++;
       }
-      cta_signal_mask(a, ch, C_S2, others);
-      // ---- cross-domain: fold the D domain partials of my shard (ascending domain id) ----
-      if (!cta_wait(a, st, F, C_S2, st.base[C_S2] + (uint64_t)(tl + 1) * rp.inc[C_S2])) break;
+    } else {  // ---- C: fold the D domain partials of my shard (ascending domain id) ----
       PtrList src, dst;
       for (int q = 0; q < D; q++) src.add(mine + (size_t)d * RG + (size_t)q * TL);
       dst.add(y + tb);
       cta_fold<T, OP>(src, dst, len);
     }
-    cta_signal_mask(a, ch, C_ACK, rp.partners);
   }
-  cta_end(st, F, rp, tl);
-}
+};
 
 // ================================================================== All-Gather (a7) ============
 // Mirror of reduce-scatter. Slot layout on a rank of domain k (RG = T + (n-d)*T/d):
 //   s_in[d][RG] | xin[n-d][T/d]
+// Stages: 0 A cross push | 1 B own shard + received pieces -> y and domain peers | 2 C peers -> y
 template <typename T>
-__global__ void __launch_bounds__(kThreads, 1) k_all_gather(const __grid_constant__ OpArgs a) {
-  constexpr int ES = sizeof(T);
-  constexpr int V = Tr<T>::V;
-  __shared__ CtaState st;
-  const int row = blockIdx.y, ch = blockIdx.x;
-  const int me = a.local_rank[row];
-  const Topo& tp = a.topo;
-  const int n = tp.n, k = tp.rank_dom[me], j = tp.rank_idx[me], d = tp.dom_size[k], D = tp.D;
-  const size_t TL = a.tile, R = a.count, Pc = TL / d, RG = TL + (size_t)(n - d) * Pc;
-  const T* x = (const T*)a.send[row];
-  T* y = (T*)a.recv[row];
-  uint64_t* F = chan_flags(a, me, ch);
-  const RankPlan& rp = a.rp[me];
-  uint32_t dpeers = 0, others = 0;
-  for (int r = 0; r < n; r++) {
-    if (r == me) continue;
-    if (tp.rank_dom[r] == k) dpeers |= 1u << r;
-    else others |= 1u << r;
+struct AgOp {
+  static constexpr int ES = sizeof(T);
+  static constexpr int V = 16 / ES;
+  const OpArgs& a;
+  const Topo& tp;
+  int me, ch, n, k, j, d, D;
+  size_t TL, R, Pc, RG;
+  const T* x;
+  T* y;
+  bool inplace;
+  __device__ AgOp(const OpArgs& a_, int row, int ch_) : a(a_), tp(a_.topo), ch(ch_) {
+    me = a.local_rank[row];
+    n = tp.n;
+    k = tp.rank_dom[me];
+    j = tp.rank_idx[me];
+    d = tp.dom_size[k];
+    D = tp.D;
+    TL = a.tile;
+    R = a.count;
+    Pc = TL / d;
+    RG = TL + (size_t)(n - d) * Pc;
+    x = (const T*)a.send[row];
+    y = (T*)a.recv[row];
+    inplace = (x == y + (size_t)me * R);
   }
-  const bool inplace = (x == y + (size_t)me * R);
-  cta_begin(st, F);
-  int tl = 0;
-  for (size_t t = ch; t < a.ntiles; t += a.nch, ++tl) {
+  __device__ int peer(int i) const { return tp.members[tp.dom_first[k] + i]; }
+  __device__ void stage(int s, size_t t, int slot) {
     const size_t tb = t * TL, len = min(TL, R - tb);
-    const int slot = tl % kNumSlots;
-    if (!cta_wait(a, st, F, C_ACK, ack_target(st, rp, tl))) break;
     T* mine = slot_ptr<T>(a, me, ch, slot);
     T* xin = mine + (size_t)d * RG;
     const size_t pj0 = sub_lo(len, d, j, V), pj1 = sub_lo(len, d, j + 1, V);
-    if (!inplace) cta_copy1<ES>(x + tb, y + (size_t)me * R + tb, len);
-    // ---- cross-domain: piece i of my shard to member i of every other domain ----
-    if (D > 1) {
+    if (s == 0) {  // ---- A: piece i of my shard to member i of every other domain ----
       for (int r = 0; r < n; r++) {
         const int q = tp.rank_dom[r];
         if (q == k) continue;
@@ -631,40 +682,28 @@ __global__ void __launch_bounds__(kThreads, 1) k_all_gather(const __grid_constan
         const size_t RGq = TL + (size_t)(n - dq) * (TL / dq);
         cta_copy1<ES>(x + tb + a0, slot_ptr<T>(a, r, ch, slot) + (size_t)dq * RGq + (size_t)ro_me * (TL / dq), a1 - a0);
       }
-      cta_signal_mask(a, ch, C_S2, others);
-      if (!cta_wait(a, st, F, C_S2, st.base[C_S2] + (uint64_t)(tl + 1) * rp.inc[C_S2])) break;
-    }
-    // ---- intra-domain: my region (own shard + received pieces) to every domain peer ----
-    {
+    } else if (s == 1) {  // ---- B: my region (own shard + received pieces) -> y and every domain peer ----
       PtrList dst_shard;
-      for (int i = 0; i < d; i++) {
-        if (i == j) continue;
-        const int peer = tp.members[tp.dom_first[k] + i];
-        dst_shard.add(slot_ptr<T>(a, peer, ch, slot) + (size_t)j * RG);
-      }
+      if (!inplace) dst_shard.add(y + (size_t)me * R + tb);
+      for (int i = 0; i < d; i++)
+        if (i != j) dst_shard.add(slot_ptr<T>(a, peer(i), ch, slot) + (size_t)j * RG);
       if (dst_shard.n) cta_copy<ES>(x + tb, dst_shard, len);
       int ro = 0;
       for (int r = 0; r < n; r++) {
         if (tp.rank_dom[r] == k) continue;
         PtrList dst;
         dst.add(y + (size_t)r * R + tb + pj0);
-        for (int i = 0; i < d; i++) {
-          if (i == j) continue;
-          const int peer = tp.members[tp.dom_first[k] + i];
-          dst.add(slot_ptr<T>(a, peer, ch, slot) + (size_t)j * RG + TL + (size_t)ro * Pc);
-        }
+        for (int i = 0; i < d; i++)
+          if (i != j) dst.add(slot_ptr<T>(a, peer(i), ch, slot) + (size_t)j * RG + TL + (size_t)ro * Pc);
         cta_copy<ES>(xin + (size_t)ro * Pc, dst, pj1 - pj0);
         ro++;
       }
-    }
-    if (d > 1) {
-      cta_signal_mask(a, ch, C_S1, dpeers);
-      if (!cta_wait(a, st, F, C_S1, st.base[C_S1] + (uint64_t)(tl + 1) * rp.inc[C_S1])) break;
+    } else {  // ---- C: every domain peer's region -> y ----
       for (int i = 0; i < d; i++) {
         if (i == j) continue;
-        const int peer = tp.members[tp.dom_first[k] + i];
+        const int pr = peer(i);
         const T* reg = mine + (size_t)i * RG;
-        cta_copy1<ES>(reg, y + (size_t)peer * R + tb, len);
+        cta_copy1<ES>(reg, y + (size_t)pr * R + tb, len);
         const size_t pi0 = sub_lo(len, d, i, V), pi1 = sub_lo(len, d, i + 1, V);
         int ro = 0;
         for (int r = 0; r < n; r++) {
@@ -674,107 +713,111 @@ __global__ void __launch_bounds__(kThreads, 1) k_all_gather(const __grid_constan
         }
       }
     }
-    cta_signal_mask(a, ch, C_ACK, rp.partners);
   }
-  cta_end(st, F, rp, tl);
-}
+};
 
 // ================================================================== Broadcast (a8) =============
 // Root -> its domain members (scatter of regions) -> one owner per other domain per segment ->
 // intra-domain all-gather. Slot layout on a rank of domain k (Rk = T/d): reg[Rk] | s3[d][Rk]
+// Stages: 0 A root scatter | 1 B cross push | 2 C region -> y and domain peers | 3 D peers -> y
 template <typename T>
-__global__ void __launch_bounds__(kThreads, 1) k_broadcast(const __grid_constant__ OpArgs a) {
-  constexpr int ES = sizeof(T);
-  constexpr int V = Tr<T>::V;
-  __shared__ CtaState st;
-  const int row = blockIdx.y, ch = blockIdx.x;
-  const int me = a.local_rank[row];
-  const Topo& tp = a.topo;
-  const int k = tp.rank_dom[me], j = tp.rank_idx[me], d = tp.dom_size[k], D = tp.D, L = tp.L;
-  const int root = a.root, kr = tp.rank_dom[root];
-  const int spj = L / d, s_lo = j * spj, s_hi = s_lo + spj;
-  const size_t TL = a.tile, Rk = TL / d;
-  const T* x = (const T*)a.send[row];
-  T* y = (T*)a.recv[row];
-  uint64_t* F = chan_flags(a, me, ch);
-  const RankPlan& rp = a.rp[me];
-  uint32_t dpeers = 0;
-  for (int i = 0; i < d; i++)
-    if (i != j) dpeers |= 1u << tp.members[tp.dom_first[k] + i];
-  const bool is_root = (me == root);
-  cta_begin(st, F);
-  int tl = 0;
-  for (size_t t = ch; t < a.ntiles; t += a.nch, ++tl) {
+struct BcOp {
+  static constexpr int ES = sizeof(T);
+  static constexpr int V = 16 / ES;
+  const OpArgs& a;
+  const Topo& tp;
+  int me, ch, k, j, d, D, L, spj, s_lo, s_hi, root, kr;
+  size_t TL, Rk;
+  const T* x;
+  T* y;
+  bool is_root;
+  __device__ BcOp(const OpArgs& a_, int row, int ch_) : a(a_), tp(a_.topo), ch(ch_) {
+    me = a.local_rank[row];
+    k = tp.rank_dom[me];
+    j = tp.rank_idx[me];
+    d = tp.dom_size[k];
+    D = tp.D;
+    L = tp.L;
+    spj = L / d;
+    s_lo = j * spj;
+    s_hi = s_lo + spj;
+    root = a.root;
+    kr = tp.rank_dom[root];
+    TL = a.tile;
+    Rk = TL / d;
+    x = (const T*)a.send[row];
+    y = (T*)a.recv[row];
+    is_root = (me == root);
+  }
+  __device__ int peer(int i) const { return tp.members[tp.dom_first[k] + i]; }
+  __device__ void stage(int s, size_t t, int slot) {
     const size_t tb = t * TL, len = min(TL, a.count - tb);
     const Geo g{len, L, 1, V};
-    const int slot = tl % kNumSlots;
-    if (!cta_wait(a, st, F, C_ACK, ack_target(st, rp, tl))) break;
     T* mine = slot_ptr<T>(a, me, ch, slot);
     const size_t r0 = g.seg(s_lo), r1 = g.seg(s_hi);
-    // ---- root scatters the regions of its domain ----
-    if (is_root && d > 1) {
+    const T* myreg = is_root ? (x + tb + r0) : mine;
+    if (s == 0) {  // ---- A: the root scatters the regions of its domain ----
+      if (!is_root) return;
       for (int i = 0; i < d; i++) {
         if (i == j) continue;
-        const int peer = tp.members[tp.dom_first[k] + i];
         const size_t p0 = g.seg(i * spj), p1 = g.seg((i + 1) * spj);
-        cta_copy1<ES>(x + tb + p0, slot_ptr<T>(a, peer, ch, slot), p1 - p0);
+        cta_copy1<ES>(x + tb + p0, slot_ptr<T>(a, peer(i), ch, slot), p1 - p0);
       }
-      cta_signal_mask(a, ch, C_S1, dpeers);
-    }
-    if (k == kr && !is_root) {
-      if (!cta_wait(a, st, F, C_S1, st.base[C_S1] + (uint64_t)(tl + 1) * rp.inc[C_S1])) break;
-    }
-    const T* myreg = is_root ? (x + tb + r0) : mine;
-    // ---- cross-domain: root-domain owners send each segment to its owner in every other domain ----
-    if (D > 1) {
-      if (k == kr) {
-        __shared__ uint32_t cnt[kMaxRanks];
-        if (threadIdx.x < kMaxRanks) cnt[threadIdx.x] = 0;
-        __syncthreads();
-        for (int s = s_lo; s < s_hi; s++) {
-          const size_t c0 = g.seg(s), c1 = g.seg(s + 1);
-          PtrList dst;
-          for (int q = 0; q < D; q++) {
-            if (q == kr) continue;
-            const int o = owner_of(tp, q, s);
-            const size_t ro = g.seg(tp.rank_idx[o] * (L / tp.dom_size[q]));
-            dst.add(slot_ptr<T>(a, o, ch, slot) + (c0 - ro));
-            if (threadIdx.x == 0) cnt[o]++;
-          }
-          cta_copy<ES>(myreg + (c0 - r0), dst, c1 - c0);
+    } else if (s == 1) {  // ---- B: root-domain owners send each segment to its owner in every other domain ----
+      if (k != kr) return;
+      for (int sg = s_lo; sg < s_hi; sg++) {
+        const size_t c0 = g.seg(sg), c1 = g.seg(sg + 1);
+        PtrList dst;
+        for (int q = 0; q < D; q++) {
+          if (q == kr) continue;
+          const int o = owner_of(tp, q, sg);
+          const size_t ro = g.seg(tp.rank_idx[o] * (L / tp.dom_size[q]));
+          dst.add(slot_ptr<T>(a, o, ch, slot) + (c0 - ro));
         }
-        cta_signal(a, ch, C_S2, cnt);
-      } else {
-        if (!cta_wait(a, st, F, C_S2, st.base[C_S2] + (uint64_t)(tl + 1) * rp.inc[C_S2])) break;
+        cta_copy<ES>(myreg + (c0 - r0), dst, c1 - c0);
       }
-    }
-    // ---- intra-domain all-gather of the regions (nobody sends to the root) ----
-    {
+    } else if (s == 2) {  // ---- C: my region -> y and every domain peer but the root ----
       PtrList dst;
       if (!is_root) dst.add(y + tb + r0);
       for (int i = 0; i < d; i++) {
         if (i == j) continue;
-        const int peer = tp.members[tp.dom_first[k] + i];
-        if (peer == root) continue;
-        dst.add(slot_ptr<T>(a, peer, ch, slot) + Rk + (size_t)j * Rk);
+        const int pr = peer(i);
+        if (pr == root) continue;
+        dst.add(slot_ptr<T>(a, pr, ch, slot) + Rk + (size_t)j * Rk);
       }
       if (dst.n) cta_copy<ES>(myreg, dst, r1 - r0);
       if (is_root && x != y) cta_copy1<ES>(x + tb, y + tb, len);
-    }
-    if (d > 1) {
-      cta_signal_mask(a, ch, C_S3, dpeers & ~(1u << root));
-      if (!is_root) {
-        if (!cta_wait(a, st, F, C_S3, st.base[C_S3] + (uint64_t)(tl + 1) * rp.inc[C_S3])) break;
-        for (int i = 0; i < d; i++) {
-          if (i == j) continue;
-          const size_t p0 = g.seg(i * spj), p1 = g.seg((i + 1) * spj);
-          cta_copy1<ES>(mine + Rk + (size_t)i * Rk, y + tb + p0, p1 - p0);
-        }
+    } else {  // ---- D: domain peers' regions -> y ----
+      if (is_root) return;
+      for (int i = 0; i < d; i++) {
+        if (i == j) continue;
+        const size_t p0 = g.seg(i * spj), p1 = g.seg((i + 1) * spj);
+        cta_copy1<ES>(mine + Rk + (size_t)i * Rk, y + tb + p0, p1 - p0);
       }
     }
-    cta_signal_mask(a, ch, C_ACK, rp.partners);
   }
-  cta_end(st, F, rp, tl);
+};
+
+// ================================================================== kernels ===================
+template <typename T, int OP>
+__global__ void __launch_bounds__(kThreads, 1) k_allreduce(const __grid_constant__ OpArgs a) {
+  ArOp<T, OP> op(a, blockIdx.y, blockIdx.x);
+  run_pipeline(a, op, op.me, blockIdx.x);
+}
+template <typename T, int OP>
+__global__ void __launch_bounds__(kThreads, 1) k_reduce_scatter(const __grid_constant__ OpArgs a) {
+  RsOp<T, OP> op(a, blockIdx.y, blockIdx.x);
+  run_pipeline(a, op, op.me, blockIdx.x);
+}
+template <typename T>
+__global__ void __launch_bounds__(kThreads, 1) k_all_gather(const __grid_constant__ OpArgs a) {
+  AgOp<T> op(a, blockIdx.y, blockIdx.x);
+  run_pipeline(a, op, op.me, blockIdx.x);
+}
+template <typename T>
+__global__ void __launch_bounds__(kThreads, 1) k_broadcast(const __grid_constant__ OpArgs a) {
+  BcOp<T> op(a, blockIdx.y, blockIdx.x);
+  run_pipeline(a, op, op.me, blockIdx.x);
 }
 
 // ================================================================== n = 1 (a9) ================
@@ -784,13 +827,13 @@ __global__ void __launch_bounds__(kThreads) k_copy(const void* src, void* dst, s
   const bool al = (((uintptr_t)src | (uintptr_t)dst) & 15) == 0;
   const size_t nv = al ? n / V : 0;
   const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x, nth = (size_t)gridDim.x * blockDim.x;
-  for (size_t v0 = tid; v0 < nv; v0 += kUnroll * nth) {
-    uint4 w[kUnroll];
+  for (size_t v0 = tid; v0 < nv; v0 += kCopyUnroll * nth) {
+    uint4 w[kCopyUnroll];
 #pragma unroll
-    for (int u = 0; u < kUnroll; u++)
+    for (int u = 0; u < kCopyUnroll; u++)
       if (v0 + u * nth < nv) w[u] = ld_v4((const char*)src + (v0 + u * nth) * 16);
 #pragma unroll
-    for (int u = 0; u < kUnroll; u++)
+    for (int u = 0; u < kCopyUnroll; u++)
       if (v0 + u * nth < nv) st_v4((char*)dst + (v0 + u * nth) * 16, w[u]);
   }
   for (size_t i = nv * V + tid; i < n; i += nth) {
@@ -834,18 +877,15 @@ cudaError_t launch_collective(const OpArgs& a, int nlocal, int dt, int red, bool
   KernFn fn = pick(a.op, dt, red);
   if (!fn) return cudaErrorInvalidValue;
   dim3 grid(a.nch, nlocal), block(kThreads);
-  if (cooperative) {
-    void* args[] = {(void*)&a};
-    return cudaLaunchCooperativeKernel((const void*)fn, grid, block, args, 0, s);
-  }
   void* args[] = {(void*)&a};
+  if (cooperative) return cudaLaunchCooperativeKernel((const void*)fn, grid, block, args, 0, s);
   return cudaLaunchKernel((const void*)fn, grid, block, args, 0, s);
 }
 
 cudaError_t launch_copy(const void* src, void* dst, size_t n, int es, cudaStream_t s) {
   if (n == 0 || src == dst) return cudaSuccess;
   size_t bytes = n * es;
-  int blocks = (int)std::min<size_t>(148 * 4, (bytes + 16 * kThreads * kUnroll - 1) / (16 * kThreads * kUnroll));
+  int blocks = (int)std::min<size_t>(148 * 2, (bytes + 16 * kThreads * kCopyUnroll - 1) / (16 * kThreads * kCopyUnroll));
   if (blocks < 1) blocks = 1;
   if (es == 4) k_copy<4><<<blocks, kThreads, 0, s>>>(src, dst, n);
   else k_copy<2><<<blocks, kThreads, 0, s>>>(src, dst, n);

@@ -76,7 +76,7 @@ size_t slot_mult_num(const Topo& t, int op, size_t tile) {
 
 static size_t default_tile_bytes(int op, int n) {
   const char* e = getenv("HETCCL_TILE_KB");
-  size_t b = e ? (size_t)atol(e) * 1024 : (size_t)512 * 1024;
+  size_t b = e ? (size_t)atol(e) * 1024 : (size_t)256 * 1024;
   if (op == OP_REDUCE_SCATTER || op == OP_ALL_GATHER) b /= (size_t)n;  // RS/AG tiles are per shard
   return std::max<size_t>(b, 4096);
 }
@@ -119,55 +119,119 @@ static int owner_of(const Topo& t, int q, int s) {  // domain q's owner of eleme
   return t.members[t.dom_first[q] + s / (t.L / dq)];
 }
 
-void make_rank_plan(const Topo& t, int op, int rank, int root, RankPlan* rp) {
-  std::memset(rp, 0, sizeof(*rp));
+// Logical stages of each op, in dataflow order (a producer stage always precedes its consumer):
+//   AR : A intra push (a1) | B intra fold + cross push (a1/a2) | C cross fold + cross AG (a2) |
+//        D intra AG push (a3) | E intra copy-out (a3)
+//   RS : A intra push | B domain fold + cross push | C cross fold                       (a6)
+//   AG : A cross push | B intra push + copy-out of cross pieces | C intra copy-out     (a7)
+//   BC : A root scatter | B cross push | C intra push + copy-out | D intra copy-out     (a8)
+// A logical stage is ACTIVE when any rank has work in it (a function of the map and root only, so
+// every rank drops the same stages); active stages are packed into pipeline positions 0..P-1.
+namespace {
+struct StageSpec {
+  bool active;
+  int wait_ctr;
+  uint32_t wait_mask;
+  int sig_ctr;
+  uint32_t sig_mask;
+};
+}  // namespace
+
+static int op_spec(const Topo& t, int op, int rank, int root, StageSpec st[kMaxStages]) {
+  std::memset(st, 0, sizeof(StageSpec) * kMaxStages);
+  for (int s = 0; s < kMaxStages; s++) st[s].wait_ctr = st[s].sig_ctr = C_NONE;
   const int k = t.rank_dom[rank], j = t.rank_idx[rank], d = t.dom_size[k], D = t.D, L = t.L, n = t.n;
-  uint32_t peers = 0;
-  for (int i = 0; i < d; i++)
-    if (i != j) peers |= 1u << t.members[t.dom_first[k] + i];
+  const bool any_intra = D < n, any_cross = D > 1;
+  uint32_t dpeers = 0, others = 0;
+  for (int r = 0; r < n; r++) {
+    if (r == rank) continue;
+    if (t.rank_dom[r] == k) dpeers |= 1u << r;
+    else others |= 1u << r;
+  }
   const int spj = L / d;
   switch (op) {
     case OP_ALLREDUCE: {
-      uint32_t cross = 0;
+      uint32_t cross = 0;  // owners of my segments in the other domains (symmetric relation)
       for (int s = j * spj; s < (j + 1) * spj; s++)
         for (int q = 0; q < D; q++)
           if (q != k) cross |= 1u << owner_of(t, q, s);
-      rp->partners = peers | cross;
-      rp->inc[C_S1] = (uint32_t)(d - 1);
-      rp->inc[C_S2] = (uint32_t)((D - 1) * spj);
-      rp->inc[C_AG] = (uint32_t)((D - 1) * spj);
-      rp->inc[C_S3] = (uint32_t)(d - 1);
-      break;
+      st[0] = {any_intra, C_NONE, 0, C_S1, dpeers};
+      st[1] = {true, C_S1, dpeers, C_S2, cross};
+      st[2] = {any_cross, C_S2, cross, C_AG, cross};
+      st[3] = {true, C_AG, cross, C_S3, dpeers};
+      st[4] = {any_intra, C_S3, dpeers, C_NONE, 0};
+      return 5;
     }
     case OP_REDUCE_SCATTER:
-    case OP_ALL_GATHER: {
-      rp->partners = ((n == 32 ? 0u : (1u << n)) - 1u) & ~(1u << rank);
-      rp->inc[C_S1] = (uint32_t)(d - 1);
-      rp->inc[C_S2] = (uint32_t)(n - d);  // one piece from every other-domain rank
-      break;
-    }
+      st[0] = {any_intra, C_NONE, 0, C_S1, dpeers};
+      st[1] = {true, C_S1, dpeers, C_S2, others};
+      st[2] = {any_cross, C_S2, others, C_NONE, 0};
+      return 3;
+    case OP_ALL_GATHER:
+      st[0] = {any_cross, C_NONE, 0, C_S2, others};
+      st[1] = {true, C_S2, others, C_S1, dpeers};
+      st[2] = {any_intra, C_S1, dpeers, C_NONE, 0};
+      return 3;
     case OP_BROADCAST: {
       const int kr = t.rank_dom[root];
-      uint32_t cross = 0;
-      if (D > 1) {
-        if (k == kr) {  // my region's segments go to every other domain's owners
-          for (int s = j * spj; s < (j + 1) * spj; s++)
-            for (int q = 0; q < D; q++)
-              if (q != kr) cross |= 1u << owner_of(t, q, s);
-        } else {  // my region's segments come from root-domain owners
-          for (int s = j * spj; s < (j + 1) * spj; s++) cross |= 1u << owner_of(t, kr, s);
+      const bool in_root_dom = (k == kr), is_root = (rank == root);
+      uint32_t bcross = 0;
+      for (int s = j * spj; s < (j + 1) * spj; s++) {
+        if (in_root_dom) {
+          for (int q = 0; q < D; q++)
+            if (q != kr) bcross |= 1u << owner_of(t, q, s);
+        } else {
+          bcross |= 1u << owner_of(t, kr, s);
         }
       }
-      rp->partners = peers | cross;
-      rp->inc[C_S1] = (k == kr && rank != root) ? 1u : 0u;             // region from the root
-      rp->inc[C_S2] = (k != kr) ? (uint32_t)spj : 0u;                    // one signal per segment
-      rp->inc[C_S3] = (rank == root) ? 0u : (uint32_t)(d - 1);            // every peer's region but mine
-      break;
+      const uint32_t root_bit = 1u << root;
+      st[0] = {t.dom_size[kr] > 1, C_NONE, 0, C_S1, is_root ? dpeers : 0u};
+      st[1] = {any_cross || t.dom_size[kr] > 1, C_S1, (in_root_dom && !is_root) ? root_bit : 0u, C_S2, in_root_dom ? bcross : 0u};
+      st[2] = {true, C_S2, in_root_dom ? 0u : bcross, C_S3, dpeers & ~root_bit};
+      st[3] = {any_intra, C_S3, is_root ? 0u : dpeers, C_NONE, 0};
+      return 4;
     }
     default:
-      break;
+      return 0;
   }
-  rp->inc[C_ACK] = (uint32_t)__builtin_popcount(rp->partners);
+}
+
+int op_stages(int op) {
+  switch (op) {
+    case OP_ALLREDUCE: return 5;
+    case OP_BROADCAST: return 4;
+    case OP_REDUCE_SCATTER:
+    case OP_ALL_GATHER: return 3;
+  }
+  return 0;
+}
+
+// Packs the active logical stages into positions; the kernel maps position -> logical stage with
+// the same rule (active flags are identical on every rank). Returns the number of positions.
+void make_rank_plan(const Topo& t, int op, int rank, int root, RankPlan* rp) {
+  std::memset(rp, 0, sizeof(*rp));
+  StageSpec st[kMaxStages];
+  const int nl = op_spec(t, op, rank, root, st);
+  for (int s = 0; s < kMaxStages; s++) rp->wait_ctr[s] = rp->sig_ctr[s] = C_NONE;
+  for (int s = 0; s < nl; s++) {
+    // positions are indexed by LOGICAL stage; inactive stages get no waits/signals and are skipped
+    if (!st[s].active) continue;
+    rp->wait_ctr[s] = (uint8_t)(st[s].wait_mask ? st[s].wait_ctr : C_NONE);
+    rp->wait_mask[s] = (uint16_t)st[s].wait_mask;
+    rp->sig_ctr[s] = (uint8_t)(st[s].sig_mask ? st[s].sig_ctr : C_NONE);
+    rp->sig_mask[s] = (uint16_t)st[s].sig_mask;
+    rp->writes |= (uint16_t)st[s].sig_mask;
+  }
+}
+
+// Bitmask of the logical stages of op that are active for this map/root (same on every rank).
+uint32_t active_stages(const Topo& t, int op, int root) {
+  StageSpec st[kMaxStages];
+  const int nl = op_spec(t, op, 0, root, st);
+  uint32_t m = 0;
+  for (int s = 0; s < nl; s++)
+    if (st[s].active) m |= 1u << s;
+  return m;
 }
 
 // Algorithmic bytes sent/received over the peer fabric by `rank` for one op, by walking the same

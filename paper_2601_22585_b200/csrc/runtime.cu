@@ -29,7 +29,7 @@ struct hetcclComm {
   int n = 0, rank = 0, device = 0;
   int map[kMaxRanks] = {0};
   Topo topo{};
-  int nch_max = 32;
+  int nch_max = 128;
   size_t slot_bytes = 0;
   size_t alloc_bytes = 0;
   char* local[kMaxRanks] = {nullptr};    // allocations owned by this comm (mux: one per rank)
@@ -80,8 +80,8 @@ long env_long(const char* name, long dflt) {
 }
 
 void read_env(hetcclComm* c) {
-  c->nch_max = (int)std::max(1L, std::min((long)kMaxChannels, env_long("HETCCL_NCHANNELS", 32)));
-  c->slot_bytes = (size_t)std::max(64L, env_long("HETCCL_SLOT_KB", 2048)) * 1024;
+  c->nch_max = (int)std::max(1L, std::min((long)kMaxChannels, env_long("HETCCL_NCHANNELS", 128)));
+  c->slot_bytes = (size_t)std::max(64L, env_long("HETCCL_SLOT_KB", 768)) * 1024;
   c->slot_bytes = (c->slot_bytes + 255) / 256 * 256;
   c->timeout_ns = (long long)std::max(1L, env_long("HETCCL_TIMEOUT_S", 30)) * 1000000000LL;
   c->alloc_bytes = kFlagsReserve + (size_t)c->nch_max * kNumSlots * c->slot_bytes;
@@ -191,6 +191,7 @@ hetcclResult_t run_op(hetcclComm_t c, int op, const void* const* sends, void* co
   a.slot_elems = slot_elems;
   a.root = root;
   a.op = op;
+  a.active = active_stages(c->topo, op, root);
   a.err = c->err;
   a.timeout_ns = c->timeout_ns;
   CUDA_TRY(c, launch_collective(a, nlocal, dt, red, c->kind == KIND_MUX, stream));
@@ -492,6 +493,28 @@ hetcclResult_t hetccl_plan_info(int nranks, const int* rank_to_domain, int rank,
   info->ntiles = g.ntiles;
   info->nchannels = g.nch;
   info->nslots = kNumSlots;
+  return hetcclSuccess;
+}
+
+hetcclResult_t hetccl_plan_stages(int nranks, const int* rank_to_domain, int rank, int op, int root,
+                                  hetcclStagePlan_t* plan) {
+  Topo t;
+  if (!plan || build_topo(nranks, rank_to_domain, &t) || rank < 0 || rank >= nranks || op < 0 || op > 3 ||
+      (op == OP_BROADCAST && (root < 0 || root >= nranks)))
+    return hetcclInvalidArgument;
+  RankPlan rp;
+  make_rank_plan(t, op, rank, root, &rp);
+  memset(plan, 0, sizeof(*plan));
+  plan->nstages = op_stages(op);
+  plan->active = active_stages(t, op, root);
+  for (int s = 0; s < 8; s++) plan->wait_ctr[s] = plan->sig_ctr[s] = C_NONE;
+  for (int s = 0; s < kMaxStages; s++) {
+    plan->wait_ctr[s] = rp.wait_ctr[s];
+    plan->wait_mask[s] = rp.wait_mask[s];
+    plan->sig_ctr[s] = rp.sig_ctr[s];
+    plan->sig_mask[s] = rp.sig_mask[s];
+  }
+  plan->writes = rp.writes;
   return hetcclSuccess;
 }
 

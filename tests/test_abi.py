@@ -137,3 +137,63 @@ def test_single_domain_has_no_cross_traffic_and_singletons_no_intra(hc):
     assert one["bytes_sent"] == S * 3 // 2
     sing = hc.hetccl_plan_info([0, 1, 2, 3], 0, hc.OP_ALLREDUCE, count, hc.FLOAT32)
     assert sing["bytes_sent"] == S * 3 // 2
+
+
+# ------------------------------------------------------------------ pipeline schedule (host plan)
+SCHED_MAPS = [[0, 1], [0, 0], [0, 0, 1, 1], [0, 1, 1, 1], [0, 1, 2, 2], [0, 0, 0, 0], [0, 1, 2, 3],
+              [0, 0, 0, 0, 1, 1, 1, 1], [0, 0, 1, 1, 1, 1, 1, 1], [0, 0, 1, 1, 2, 2, 2, 2], [1, 0, 1, 0, 2, 2],
+              [0, 0, 0, 1, 1, 1, 1, 1], [0, 1, 1, 2, 2, 2], [0] * 8, list(range(8)), [0, 1] * 8]
+
+
+@pytest.mark.parametrize("m", SCHED_MAPS, ids=lambda m: "".join(map(str, m)))
+@pytest.mark.parametrize("op", [0, 1, 2, 3])
+def test_schedule_is_symmetric_and_acyclic(hc, m, op):
+    """The flag protocol's invariants (kernels.cu run_pipeline): every signal a rank sends is awaited
+    by its receiver on the same counter, every wait has a sender, a producer stage always precedes
+    its consumer (so no iteration waits on itself), each counter has one consumer stage, active
+    stages agree on every rank, and `writes` covers every rank signalled."""
+    n = len(m)
+    roots = range(n) if op == 3 else [0]
+    for root in roots:
+        plans = [hc.hetccl_plan_stages(m, r, op, root) for r in range(n)]
+        assert len({p["active"] for p in plans}) == 1
+        act = plans[0]["active"]
+        for w, pw in enumerate(plans):
+            consumers = {}
+            for s in range(pw["nstages"]):
+                if pw["wait_ctr"][s] != 7:
+                    assert (act >> s) & 1
+                    assert pw["wait_ctr"][s] not in consumers, "two stages wait on one counter"
+                    consumers[pw["wait_ctr"][s]] = s
+            for s in range(pw["nstages"]):
+                c, mask = pw["sig_ctr"][s], pw["sig_mask"][s]
+                if c == 7:
+                    assert mask == 0
+                    continue
+                assert (act >> s) & 1
+                assert not (mask >> w) & 1, "no self signal"
+                assert (pw["writes"] & mask) == mask
+                for r in range(n):
+                    if not (mask >> r) & 1:
+                        continue
+                    pr = plans[r]
+                    cons = [s2 for s2 in range(pr["nstages"]) if pr["wait_ctr"][s2] == c]
+                    assert len(cons) == 1, f"rank {r} never waits on counter {c}"
+                    assert (pr["wait_mask"][cons[0]] >> w) & 1, f"rank {r} does not expect {w} on {c}"
+                    assert cons[0] > s, "consumer must follow producer"
+            for s in range(pw["nstages"]):
+                c, mask = pw["wait_ctr"][s], pw["wait_mask"][s]
+                for r in range(n):
+                    if (mask >> r) & 1:
+                        ps = plans[r]
+                        assert any(ps["sig_ctr"][s2] == c and (ps["sig_mask"][s2] >> w) & 1
+                                   for s2 in range(ps["nstages"])), f"{w} waits on {r} that never signals {c}"
+
+
+def test_schedule_stage_sets(hc):
+    # 1+1: no intra stages; one domain: no cross stage; singletons of 4: no intra stages
+    assert hc.hetccl_plan_stages([0, 1], 0, 0)["active"] == 0b01110
+    assert hc.hetccl_plan_stages([0, 0, 0, 0], 0, 0)["active"] == 0b11011
+    assert hc.hetccl_plan_stages([0, 0, 1, 1], 0, 0)["active"] == 0b11111
+    assert hc.hetccl_plan_stages([0, 1, 2, 3], 0, 1)["active"] == 0b110  # RS: B, C
+    assert hc.hetccl_plan_stages([0, 1, 2, 3], 0, 2)["active"] == 0b011  # AG: A, B
