@@ -302,21 +302,19 @@ __device__ __forceinline__ T* slot_ptr(const OpArgs& a, int rank, int ch, int sl
 
 __device__ __forceinline__ size_t floor_to(size_t x, size_t q) { return x / q * q; }
 
-// elementary-segment and piece boundaries of one AR tile (same formulas as plan.cpp)
+// Elementary-segment and piece boundaries of one AR/BC tile (same formulas as plan.cpp): the grid
+// of a FULL tile (segment = T/L, piece = T/(L*D) elements, multiples of the vector width because T
+// is a multiple of L*D*V) clipped to the tile's length, so no piece of a ragged last tile is ever
+// longer than its scratch slot.
 struct Geo {
-  size_t len;
-  int L, D, V;
-  __device__ size_t seg(int s) const { return s >= L ? len : floor_to(len * (size_t)s / L, V); }
-  __device__ size_t piece(int s, int p) const {
-    size_t b0 = seg(s), b1 = seg(s + 1);
-    return p >= D ? b1 : b0 + floor_to((b1 - b0) * (size_t)p / D, V);
-  }
+  size_t len, T;
+  int L, D;
+  __device__ size_t seg(int s) const { return min(len, (size_t)s * (T / L)); }
+  __device__ size_t piece(int s, int p) const { return min(seg(s + 1), seg(s) + (size_t)p * (T / L / D)); }
 };
 
-// piece i of dd of a shard tile of length len (RS / AG)
-__device__ __forceinline__ size_t sub_lo(size_t len, int dd, int i, int V) {
-  return i >= dd ? len : floor_to(len * (size_t)i / dd, V);
-}
+// piece i of dd of a shard tile (RS / AG): full-tile grid T/dd clipped to len
+__device__ __forceinline__ size_t sub_lo(size_t len, size_t T, int dd, int i) { return min(len, (size_t)i * (T / dd)); }
 
 __device__ __forceinline__ int owner_of(const Topo& t, int q, int s) {
   return t.members[t.dom_first[q] + s / (t.L / t.dom_size[q])];
@@ -479,7 +477,7 @@ struct ArOp {
   }
   __device__ void stage(int s, size_t t, int slot) {
     const size_t tb = t * TL, len = min(TL, a.count - tb);
-    const Geo g{len, L, D, V};
+    const Geo g{len, TL, L, D};
     const size_t r0 = g.seg(s_lo), r1 = g.seg(s_hi);
     T* mine = slot_ptr<T>(a, me, ch, slot);
     T* my_ag = mine + TL + (size_t)D * Rk;
@@ -588,14 +586,14 @@ struct RsOp {
   __device__ void stage(int s, size_t t, int slot) {
     const size_t tb = t * TL, len = min(TL, R - tb);
     T* mine = slot_ptr<T>(a, me, ch, slot);
-    const size_t pj0 = sub_lo(len, d, j, V), pj1 = sub_lo(len, d, j + 1, V);
+    const size_t pj0 = sub_lo(len, TL, d, j), pj1 = sub_lo(len, TL, d, j + 1);
     if (s == 0) {  // ---- A: each domain peer gets my data for its region ----
       for (int i = 0; i < d; i++) {
         if (i == j) continue;
         const int pr = tp.members[tp.dom_first[k] + i];
         T* dst = slot_ptr<T>(a, pr, ch, slot) + (size_t)j * RG;
         cta_copy1<ES>(x + (size_t)pr * R + tb, dst, len);
-        const size_t pi0 = sub_lo(len, d, i, V), pi1 = sub_lo(len, d, i + 1, V);
+        const size_t pi0 = sub_lo(len, TL, d, i), pi1 = sub_lo(len, TL, d, i + 1);
         int ro = 0;
         for (int r = 0; r < n; r++) {
           if (tp.rank_dom[r] == k) continue;
@@ -669,7 +667,7 @@ struct AgOp {
     const size_t tb = t * TL, len = min(TL, R - tb);
     T* mine = slot_ptr<T>(a, me, ch, slot);
     T* xin = mine + (size_t)d * RG;
-    const size_t pj0 = sub_lo(len, d, j, V), pj1 = sub_lo(len, d, j + 1, V);
+    const size_t pj0 = sub_lo(len, TL, d, j), pj1 = sub_lo(len, TL, d, j + 1);
     if (s == 0) {  // ---- A: piece i of my shard to member i of every other domain ----
       for (int r = 0; r < n; r++) {
         const int q = tp.rank_dom[r];
@@ -678,7 +676,7 @@ struct AgOp {
         int ro_me = 0;  // my index among the ranks outside domain q
         for (int r2 = 0; r2 < me; r2++)
           if (tp.rank_dom[r2] != q) ro_me++;
-        const size_t a0 = sub_lo(len, dq, i, V), a1 = sub_lo(len, dq, i + 1, V);
+        const size_t a0 = sub_lo(len, TL, dq, i), a1 = sub_lo(len, TL, dq, i + 1);
         const size_t RGq = TL + (size_t)(n - dq) * (TL / dq);
         cta_copy1<ES>(x + tb + a0, slot_ptr<T>(a, r, ch, slot) + (size_t)dq * RGq + (size_t)ro_me * (TL / dq), a1 - a0);
       }
@@ -704,7 +702,7 @@ struct AgOp {
         const int pr = peer(i);
         const T* reg = mine + (size_t)i * RG;
         cta_copy1<ES>(reg, y + (size_t)pr * R + tb, len);
-        const size_t pi0 = sub_lo(len, d, i, V), pi1 = sub_lo(len, d, i + 1, V);
+        const size_t pi0 = sub_lo(len, TL, d, i), pi1 = sub_lo(len, TL, d, i + 1);
         int ro = 0;
         for (int r = 0; r < n; r++) {
           if (tp.rank_dom[r] == k) continue;
@@ -752,7 +750,7 @@ struct BcOp {
   __device__ int peer(int i) const { return tp.members[tp.dom_first[k] + i]; }
   __device__ void stage(int s, size_t t, int slot) {
     const size_t tb = t * TL, len = min(TL, a.count - tb);
-    const Geo g{len, L, 1, V};
+    const Geo g{len, TL, L, 1};
     T* mine = slot_ptr<T>(a, me, ch, slot);
     const size_t r0 = g.seg(s_lo), r1 = g.seg(s_hi);
     const T* myreg = is_root ? (x + tb + r0) : mine;

@@ -3,11 +3,12 @@
 // kernels.cu execute exactly this partition (the boundary formulas are restated there on the device).
 //
 // Partition of one AR tile of `len` elements:
-//   L = lcm(d_0..d_{D-1}) elementary segments, boundary b(s) = floor_V(len*s/L), b(L) = len
-//   (floor_V rounds down to a multiple of the 16-byte vector width V), so member j of domain k
-//   (size d) owns segments [j*L/d, (j+1)*L/d) and every segment has exactly one owner per domain
-//   (SURVEY §8(a) a0). Piece p of segment s (reduced by domain p's owner in the cross stage):
-//   c(s,p) = b(s) + floor_V((b(s+1)-b(s))*p/D), c(s,D) = b(s+1).
+//   L = lcm(d_0..d_{D-1}) elementary segments on the grid of a FULL tile T (a multiple of L*D*V,
+//   V = 16-byte vector width), clipped to len: b(s) = min(len, s*T/L). Member j of domain k (size
+//   d) owns segments [j*L/d, (j+1)*L/d), so every segment has exactly one owner per domain (SURVEY
+//   §8(a) a0). Piece p of segment s (reduced by domain p's owner in the cross stage):
+//   c(s,p) = min(b(s+1), b(s) + p*T/(L*D)). Clipping (rather than rescaling to len) keeps every
+//   piece of a ragged last tile within its scratch slot and every boundary V-aligned.
 #include <algorithm>
 #include <cstring>
 
@@ -246,18 +247,15 @@ void plan_bytes(const Topo& t, int op, int rank, int root, size_t count, int es,
   size_t S = 0, R = 0;
   for (size_t ti = 0; ti < g.ntiles; ti++) {
     size_t len = std::min(g.tile, count - ti * g.tile);
-    auto seg = [&](int s) -> size_t { return s >= L ? len : floor_to(len * (size_t)s / L, V); };
-    auto piece = [&](int s, int p) -> size_t {
-      size_t b0 = seg(s), b1 = seg(s + 1);
-      return p >= D ? b1 : b0 + floor_to((b1 - b0) * (size_t)p / D, V);
-    };
+    // full-tile grid clipped to len (kernels.cu Geo / sub_lo)
+    auto seg = [&](int s) -> size_t { return std::min(len, (size_t)s * (tile / L)); };
+    auto piece = [&](int s, int p) -> size_t { return std::min(seg(s + 1), seg(s) + (size_t)p * (tile / L / D)); };
     auto region = [&](int q, int m) -> size_t {  // region length of member m of domain q
       int sp = L / t.dom_size[q];
       return seg((m + 1) * sp) - seg(m * sp);
     };
     auto sub = [&](size_t l, int dd, int i) -> size_t {  // piece i of dd of a shard tile of length l
-      size_t a = floor_to(l * (size_t)i / dd, V), b = (i + 1 >= dd) ? l : floor_to(l * (size_t)(i + 1) / dd, V);
-      return b - a;
+      return std::min(l, (size_t)(i + 1) * (tile / dd)) - std::min(l, (size_t)i * (tile / dd));
     };
     if (op == OP_ALLREDUCE) {
       const int spj = L / d;

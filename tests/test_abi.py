@@ -73,7 +73,9 @@ def test_allreduce_bytes_closed_form(hc, name):
     """Per-rank AR bytes = S*(2(d-1)/d + 2(D-1)/(D d)) for a count divisible by everything."""
     m = SPLITS[name]
     n, D = len(m), max(m) + 1
-    count = 8 * 840 * 64 * 1024  # divisible by every L*D*V here
+    # a whole number of full tiles (the ragged last tile is split on the clipped full-tile grid, DESIGN.md §2)
+    tile = hc.hetccl_plan_info(m, 0, hc.OP_ALLREDUCE, 1 << 30, hc.BFLOAT16)["tile_elems"]
+    count = tile * 1000
     S = count * 2
     busiest = 0
     for r in range(n):
@@ -93,7 +95,8 @@ def test_rs_ag_bytes_closed_form(hc, name):
     """RS received per rank = (d-1)/d*S + (D-1)*S/n; AG is the mirror (sent = that); SURVEY §8(d)."""
     m = SPLITS[name]
     n, D = len(m), max(m) + 1
-    R = 840 * 64 * 1024  # recvcount
+    tile = hc.hetccl_plan_info(m, 0, hc.OP_REDUCE_SCATTER, 1 << 28, hc.BFLOAT16)["tile_elems"]
+    R = tile * 1000  # recvcount: whole tiles
     S = n * R * 2
     for r in range(n):
         d = m.count(m[r])
