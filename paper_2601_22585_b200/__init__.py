@@ -47,7 +47,7 @@ EXPORTED = [
     "hetccl_comm_get_async_error", "hetccl_get_error_string", "hetccl_get_last_error", "hetccl_allreduce",
     "hetccl_reduce_scatter", "hetccl_all_gather", "hetccl_broadcast", "hetccl_mux_allreduce",
     "hetccl_mux_reduce_scatter", "hetccl_mux_all_gather", "hetccl_mux_broadcast", "hetccl_plan_info",
-    "hetccl_plan_stages",
+    "hetccl_plan_stages", "hetccl_comm_get_trace",
 ]
 
 _lib = None
@@ -84,6 +84,7 @@ def lib():
         "hetccl_mux_broadcast": [pp, pp, c_size, c_int, c_int, vp, vp],
         "hetccl_plan_info": [c_int, ip, c_int, c_int, c_size, c_int, c_int, c_int, ctypes.POINTER(PlanInfo)],
         "hetccl_plan_stages": [c_int, ip, c_int, c_int, c_int, ctypes.POINTER(StagePlan)],
+        "hetccl_comm_get_trace": [vp, vp, c_size, ip],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -186,6 +187,19 @@ def hetccl_comm_info(comm):
 
 def hetccl_comm_get_async_error(comm):
     _check(lib().hetccl_comm_get_async_error(comm), comm)
+
+
+def hetccl_comm_get_trace(comm):
+    """Per-iteration timestamps of the last op (HETCCL_TRACE_ITERS at comm creation): numpy uint64
+    array [local ranks, channels, iterations, 4] (wait start, work start, work end, fenced), or None."""
+    import numpy as np
+    shape = (ctypes.c_int * 3)()
+    _check(lib().hetccl_comm_get_trace(comm, None, 0, shape), comm)
+    if shape[0] == 0:
+        return None
+    out = np.zeros((shape[0], shape[1], shape[2], 4), np.uint64)
+    _check(lib().hetccl_comm_get_trace(comm, out.ctypes.data, out.nbytes, shape), comm)
+    return out
 
 
 def hetccl_plan_info(rank_to_domain, rank, op, count, dtype=BFLOAT16, root=0, nchannels=0):

@@ -88,6 +88,8 @@ struct OpArgs {
   int op;
   unsigned long long* err;      // device error word of the comm
   long long timeout_ns;
+  unsigned long long* trace;    // optional per-iteration timestamps (HETCCL_TRACE_ITERS), else null
+  int trace_iters;
 };
 
 // ---- host plan (plan.cpp) ----

@@ -361,7 +361,11 @@ __device__ __forceinline__ void run_pipeline(const OpArgs& a, Op& op, int me, in
   const long long ntl = (ch < (long long)a.ntiles) ? ((long long)a.ntiles - ch + a.nch - 1) / a.nch : 0;
   const unsigned long long tiles0 = ps.tiles0;
   const int lane = threadIdx.x & 31;
+  unsigned long long* trc = nullptr;  // [it][4] globaltimer stamps: wait start, work start, work end, fenced
+  if (a.trace) trc = a.trace + ((size_t)blockIdx.y * gridDim.x + ch) * (size_t)a.trace_iters * 4;
   for (long long it = 0; it < ntl + np - 1; ++it) {
+    const bool tr = trc && threadIdx.x == 0 && it < a.trace_iters;
+    if (tr) trc[it * 4 + 0] = globaltimer();
     // ---- 1. waits (warp 0; lane = sender) ----
     if (threadIdx.x < 32) {
       bool ok = true;
@@ -403,6 +407,7 @@ __device__ __forceinline__ void run_pipeline(const OpArgs& a, Op& op, int me, in
     }
     __syncthreads();
     if (*(volatile int*)&ps.abort_) break;
+    if (tr) trc[it * 4 + 1] = globaltimer();
     // ---- 2. stage work ----
     for (int p = 0; p < np; p++) {
       const long long tl = it - p;
@@ -410,9 +415,11 @@ __device__ __forceinline__ void run_pipeline(const OpArgs& a, Op& op, int me, in
       op.stage(stage_at[p], (size_t)ch + (size_t)tl * a.nch, (int)((tiles0 + tl) % kNumSlots));
     }
     __syncthreads();
+    if (tr) trc[it * 4 + 2] = globaltimer();
     // ---- 3. release: fence, then signals ----
     if (threadIdx.x < 32) {
       fence_acq_rel_sys();
+      if (tr) trc[it * 4 + 3] = globaltimer();
       if (lane < n && lane != me) {
         for (int p = 0; p < np; p++) {
           const long long tl = it - p;

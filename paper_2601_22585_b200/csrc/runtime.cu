@@ -38,6 +38,10 @@ struct hetcclComm {
   unsigned long long* err = nullptr;     // device error word
   bool connected = false;
   long long timeout_ns = 30LL * 1000000000LL;
+  int trace_iters = 0;                    // HETCCL_TRACE_ITERS: per-iteration timestamps of the last op
+  unsigned long long* trace = nullptr;
+  size_t trace_bytes = 0;
+  int trace_shape[2] = {0, 0};            // local ranks, channels of the last traced op
   std::string last_error;
 };
 
@@ -84,6 +88,7 @@ void read_env(hetcclComm* c) {
   c->slot_bytes = (size_t)std::max(64L, env_long("HETCCL_SLOT_KB", 768)) * 1024;
   c->slot_bytes = (c->slot_bytes + 255) / 256 * 256;
   c->timeout_ns = (long long)std::max(1L, env_long("HETCCL_TIMEOUT_S", 30)) * 1000000000LL;
+  c->trace_iters = (int)std::max(0L, std::min(4096L, env_long("HETCCL_TRACE_ITERS", 0)));
   c->alloc_bytes = kFlagsReserve + (size_t)c->nch_max * kNumSlots * c->slot_bytes;
 }
 
@@ -194,6 +199,21 @@ hetcclResult_t run_op(hetcclComm_t c, int op, const void* const* sends, void* co
   a.active = active_stages(c->topo, op, root);
   a.err = c->err;
   a.timeout_ns = c->timeout_ns;
+  if (c->trace_iters > 0) {
+    const size_t need = (size_t)nlocal * geo.nch * c->trace_iters * 4 * sizeof(unsigned long long);
+    if (need > c->trace_bytes) {
+      if (c->trace) cudaFree(c->trace);
+      c->trace = nullptr;
+      c->trace_bytes = 0;
+      CUDA_TRY(c, cudaMalloc((void**)&c->trace, need));
+      c->trace_bytes = need;
+    }
+    CUDA_TRY(c, cudaMemsetAsync(c->trace, 0, need, stream));
+    a.trace = c->trace;
+    a.trace_iters = c->trace_iters;
+    c->trace_shape[0] = nlocal;
+    c->trace_shape[1] = geo.nch;
+  }
   CUDA_TRY(c, launch_collective(a, nlocal, dt, red, c->kind == KIND_MUX, stream));
   return hetcclSuccess;
 }
@@ -389,6 +409,7 @@ hetcclResult_t hetccl_comm_destroy(hetcclComm_t c) {
       if (c->local[r]) cudaFree(c->local[r]);
     }
     if (c->err) cudaFree(c->err);
+    if (c->trace) cudaFree(c->trace);
   }
   delete c;
   return hetcclSuccess;
@@ -515,6 +536,23 @@ hetcclResult_t hetccl_plan_stages(int nranks, const int* rank_to_domain, int ran
     plan->sig_mask[s] = rp.sig_mask[s];
   }
   plan->writes = rp.writes;
+  return hetcclSuccess;
+}
+
+hetcclResult_t hetccl_comm_get_trace(hetcclComm_t c, void* host, size_t bytes, int* shape) {
+  if (!c || !shape) return hetcclInvalidArgument;
+  shape[0] = c->trace_shape[0];
+  shape[1] = c->trace_shape[1];
+  shape[2] = c->trace_iters;
+  const size_t need = (size_t)shape[0] * shape[1] * shape[2] * 4 * sizeof(unsigned long long);
+  if (!c->trace || need == 0) {
+    shape[0] = shape[1] = shape[2] = 0;
+    return hetcclSuccess;
+  }
+  if (!host || bytes < need) return fail(c, hetcclInvalidArgument, "trace buffer needs %zu bytes", need);
+  DevGuard g(c->device);
+  CUDA_TRY(c, cudaDeviceSynchronize());
+  CUDA_TRY(c, cudaMemcpy(host, c->trace, need, cudaMemcpyDeviceToHost));
   return hetcclSuccess;
 }
 
