@@ -197,7 +197,8 @@ HETCCL_API hetcclResult_t hetccl_plan_stages(int nranks, const int* rank_to_doma
  * (local rank, channel) CTA and pipeline iteration it < K, four globaltimer stamps in ns: wait start,
  * work start (all waits satisfied), work end, release fence done. This copies the LAST op's stamps to
  * `host` as uint64 [shape0 local ranks][shape1 channels][shape2 = K iterations][4] (synchronizes
- * the device; unused iterations are 0). shape[0..2] are written; all zero if tracing is off.
+ * the device; unused iterations are 0). shape[0..2] are written; all zero if tracing is off. With
+ * host == NULL only the shape is written.
  */
 HETCCL_API hetcclResult_t hetccl_comm_get_trace(hetcclComm_t comm, void* host, size_t bytes, int* shape);
 

@@ -316,6 +316,9 @@ struct Geo {
 // piece i of dd of a shard tile (RS / AG): full-tile grid T/dd clipped to len
 __device__ __forceinline__ size_t sub_lo(size_t len, size_t T, int dd, int i) { return min(len, (size_t)i * (T / dd)); }
 
+// compact index of domain member i in a buffer that has no entry for member j (the owner itself)
+__device__ __forceinline__ int cidx(int i, int j) { return i < j ? i : i - 1; }
+
 __device__ __forceinline__ int owner_of(const Topo& t, int q, int s) {
   return t.members[t.dom_first[q] + s / (t.L / t.dom_size[q])];
 }
@@ -447,8 +450,9 @@ __device__ __forceinline__ void run_pipeline(const OpArgs& a, Op& op, int me, in
 }
 
 // ================================================================== All-Reduce (a1-a5) =========
-// Slot layout on a rank of domain k (d = d_k, Rk = tile/d):
-//   s1[d][Rk] | s2[D][Rk] | ag[Rk] | s3[d][Rk]
+// Slot layout on a rank of domain k (d = d_k, Rk = tile/d; s1/s3 have one entry per domain PEER,
+// compact index cidx(i, j)):
+//   s1[d-1][Rk] | s2[D][Rk] | ag[Rk] | s3[d-1][Rk]
 // Stages: 0 A intra push | 1 B intra fold + cross push | 2 C cross fold + AG push |
 //         3 D final region -> y and domain peers | 4 E domain peers' regions -> y
 template <typename T, int OP>
@@ -477,6 +481,8 @@ struct ArOp {
     y = (T*)a.recv[row];
   }
   __device__ int peer(int i) const { return tp.members[tp.dom_first[k] + i]; }
+  // offset of s2 in the slot of a rank whose domain has dq members
+  __device__ size_t s2_off(int dq) const { return (size_t)(dq - 1) * (TL / dq); }
   // start of the region of owner o (domain q) within a tile, and o's Rk
   __device__ size_t region_lo(const Geo& g, int o) const {
     const int q = tp.rank_dom[o];
@@ -487,13 +493,14 @@ struct ArOp {
     const Geo g{len, TL, L, D};
     const size_t r0 = g.seg(s_lo), r1 = g.seg(s_hi);
     T* mine = slot_ptr<T>(a, me, ch, slot);
-    T* my_ag = mine + TL + (size_t)D * Rk;
+    T* my_s2 = mine + s2_off(d);
+    T* my_ag = my_s2 + (size_t)D * Rk;
     T* my_s3 = my_ag + Rk;
     if (s == 0) {  // ---- A: push my data for each domain peer's region to its s1[j] ----
       for (int i = 0; i < d; i++) {
         if (i == j) continue;
         const size_t p0 = g.seg(i * spj), p1 = g.seg((i + 1) * spj);
-        cta_copy1<ES>(x + tb + p0, slot_ptr<T>(a, peer(i), ch, slot) + (size_t)j * Rk, p1 - p0);
+        cta_copy1<ES>(x + tb + p0, slot_ptr<T>(a, peer(i), ch, slot) + (size_t)cidx(j, i) * Rk, p1 - p0);
       }
     } else if (s == 1) {  // ---- B: fold my region over the domain; route each piece to its reducer ----
       for (int sg = s_lo; sg < s_hi; sg++) {
@@ -502,14 +509,15 @@ struct ArOp {
           if (c1 <= c0) continue;
           PtrList src, dst;
           for (int i = 0; i < d; i++)
-            src.add(i == j ? (const void*)(x + tb + c0) : (const void*)(mine + (size_t)i * Rk + (c0 - r0)));
+            src.add(i == j ? (const void*)(x + tb + c0) : (const void*)(mine + (size_t)cidx(i, j) * Rk + (c0 - r0)));
           if (D == 1) {
             dst.add(y + tb + c0);
           } else if (q == k) {
-            dst.add(mine + TL + (size_t)k * Rk + (c0 - r0));
+            dst.add(my_s2 + (size_t)k * Rk + (c0 - r0));
           } else {
             const int o = owner_of(tp, q, sg);
-            dst.add(slot_ptr<T>(a, o, ch, slot) + TL + (size_t)k * (TL / tp.dom_size[q]) + (c0 - region_lo(g, o)));
+            const int dq = tp.dom_size[q];
+            dst.add(slot_ptr<T>(a, o, ch, slot) + s2_off(dq) + (size_t)k * (TL / dq) + (c0 - region_lo(g, o)));
           }
           cta_fold<T, OP>(src, dst, c1 - c0);
         }
@@ -519,20 +527,20 @@ struct ArOp {
         const size_t c0 = g.piece(sg, k), c1 = g.piece(sg, k + 1);
         if (c1 <= c0) continue;
         PtrList src, dst;
-        for (int q = 0; q < D; q++) src.add(mine + TL + (size_t)q * Rk + (c0 - r0));
+        for (int q = 0; q < D; q++) src.add(my_s2 + (size_t)q * Rk + (c0 - r0));
         dst.add(y + tb + c0);
         for (int q = 0; q < D; q++) {
           if (q == k) continue;
           const int o = owner_of(tp, q, sg);
           const int dq = tp.dom_size[q];
-          dst.add(slot_ptr<T>(a, o, ch, slot) + TL + (size_t)D * (TL / dq) + (c0 - region_lo(g, o)));
+          dst.add(slot_ptr<T>(a, o, ch, slot) + s2_off(dq) + (size_t)D * (TL / dq) + (c0 - region_lo(g, o)));
         }
         cta_fold<T, OP>(src, dst, c1 - c0);
       }
     } else if (s == 3) {  // ---- D: my final region -> y (pieces from other owners) and to domain peers ----
       PtrList peers_s3;
       for (int i = 0; i < d; i++)
-        if (i != j) peers_s3.add(slot_ptr<T>(a, peer(i), ch, slot) + TL + (size_t)(D + 1) * Rk + (size_t)j * Rk);
+        if (i != j) peers_s3.add(slot_ptr<T>(a, peer(i), ch, slot) + s2_off(d) + (size_t)(D + 1) * Rk + (size_t)cidx(j, i) * Rk);
       if (D == 1) {
         cta_copy<ES>(y + tb + r0, peers_s3, r1 - r0);
       } else {
@@ -555,7 +563,7 @@ struct ArOp {
       for (int i = 0; i < d; i++) {
         if (i == j) continue;
         const size_t p0 = g.seg(i * spj), p1 = g.seg((i + 1) * spj);
-        cta_copy1<ES>(my_s3 + (size_t)i * Rk, y + tb + p0, p1 - p0);
+        cta_copy1<ES>(my_s3 + (size_t)cidx(i, j) * Rk, y + tb + p0, p1 - p0);
       }
     }
   }
@@ -564,7 +572,7 @@ struct ArOp {
 // ================================================================== Reduce-Scatter (a6) ========
 // Per tile (per-shard offsets [tb, tb+len)), member j of domain k owns: its own shard, plus piece j
 // (of d) of every other-domain shard. Slot layout on a rank of domain k (RG = T + (n-d)*T/d):
-//   s1[d][RG] | s2[D][T]    (s1[i]: own-shard part at 0, other-domain shard #ro at T + ro*T/d)
+//   s1[d-1][RG] | s2[D][T]  (s1[cidx(i,j)]: own-shard part at 0, other-domain shard #ro at T + ro*T/d)
 // Stages: 0 A intra push | 1 B domain fold + cross push | 2 C cross fold -> y
 template <typename T, int OP>
 struct RsOp {
@@ -598,7 +606,7 @@ struct RsOp {
       for (int i = 0; i < d; i++) {
         if (i == j) continue;
         const int pr = tp.members[tp.dom_first[k] + i];
-        T* dst = slot_ptr<T>(a, pr, ch, slot) + (size_t)j * RG;
+        T* dst = slot_ptr<T>(a, pr, ch, slot) + (size_t)cidx(j, i) * RG;
         cta_copy1<ES>(x + (size_t)pr * R + tb, dst, len);
         const size_t pi0 = sub_lo(len, TL, d, i), pi1 = sub_lo(len, TL, d, i + 1);
         int ro = 0;
@@ -612,9 +620,9 @@ struct RsOp {
       {
         PtrList src, dst;
         for (int i = 0; i < d; i++)
-          src.add(i == j ? (const void*)(x + (size_t)me * R + tb) : (const void*)(mine + (size_t)i * RG));
+          src.add(i == j ? (const void*)(x + (size_t)me * R + tb) : (const void*)(mine + (size_t)cidx(i, j) * RG));
         if (D == 1) dst.add(y + tb);
-        else dst.add(mine + (size_t)d * RG + (size_t)k * TL);
+        else dst.add(mine + (size_t)(d - 1) * RG + (size_t)k * TL);
         cta_fold<T, OP>(src, dst, len);
       }
       int ro = 0;
@@ -623,16 +631,16 @@ struct RsOp {
         PtrList src, dst;
         for (int i = 0; i < d; i++)
           src.add(i == j ? (const void*)(x + (size_t)r * R + tb + pj0)
-                         : (const void*)(mine + (size_t)i * RG + TL + (size_t)ro * Pc));
+                         : (const void*)(mine + (size_t)cidx(i, j) * RG + TL + (size_t)ro * Pc));
         const int dr = tp.dom_size[tp.rank_dom[r]];
         const size_t RGr = TL + (size_t)(n - dr) * (TL / dr);
-        dst.add(slot_ptr<T>(a, r, ch, slot) + (size_t)dr * RGr + (size_t)k * TL + pj0);
+        dst.add(slot_ptr<T>(a, r, ch, slot) + (size_t)(dr - 1) * RGr + (size_t)k * TL + pj0);
         cta_fold<T, OP>(src, dst, pj1 - pj0);
         ro++;
       }
     } else {  // ---- C: fold the D domain partials of my shard (ascending domain id) ----
       PtrList src, dst;
-      for (int q = 0; q < D; q++) src.add(mine + (size_t)d * RG + (size_t)q * TL);
+      for (int q = 0; q < D; q++) src.add(mine + (size_t)(d - 1) * RG + (size_t)q * TL);
       dst.add(y + tb);
       cta_fold<T, OP>(src, dst, len);
     }
@@ -641,7 +649,7 @@ struct RsOp {
 
 // ================================================================== All-Gather (a7) ============
 // Mirror of reduce-scatter. Slot layout on a rank of domain k (RG = T + (n-d)*T/d):
-//   s_in[d][RG] | xin[n-d][T/d]
+//   s_in[d-1][RG] | xin[n-d][T/d]
 // Stages: 0 A cross push | 1 B own shard + received pieces -> y and domain peers | 2 C peers -> y
 template <typename T>
 struct AgOp {
@@ -673,7 +681,7 @@ struct AgOp {
   __device__ void stage(int s, size_t t, int slot) {
     const size_t tb = t * TL, len = min(TL, R - tb);
     T* mine = slot_ptr<T>(a, me, ch, slot);
-    T* xin = mine + (size_t)d * RG;
+    T* xin = mine + (size_t)(d - 1) * RG;
     const size_t pj0 = sub_lo(len, TL, d, j), pj1 = sub_lo(len, TL, d, j + 1);
     if (s == 0) {  // ---- A: piece i of my shard to member i of every other domain ----
       for (int r = 0; r < n; r++) {
@@ -685,13 +693,13 @@ struct AgOp {
           if (tp.rank_dom[r2] != q) ro_me++;
         const size_t a0 = sub_lo(len, TL, dq, i), a1 = sub_lo(len, TL, dq, i + 1);
         const size_t RGq = TL + (size_t)(n - dq) * (TL / dq);
-        cta_copy1<ES>(x + tb + a0, slot_ptr<T>(a, r, ch, slot) + (size_t)dq * RGq + (size_t)ro_me * (TL / dq), a1 - a0);
+        cta_copy1<ES>(x + tb + a0, slot_ptr<T>(a, r, ch, slot) + (size_t)(dq - 1) * RGq + (size_t)ro_me * (TL / dq), a1 - a0);
       }
     } else if (s == 1) {  // ---- B: my region (own shard + received pieces) -> y and every domain peer ----
       PtrList dst_shard;
       if (!inplace) dst_shard.add(y + (size_t)me * R + tb);
       for (int i = 0; i < d; i++)
-        if (i != j) dst_shard.add(slot_ptr<T>(a, peer(i), ch, slot) + (size_t)j * RG);
+        if (i != j) dst_shard.add(slot_ptr<T>(a, peer(i), ch, slot) + (size_t)cidx(j, i) * RG);
       if (dst_shard.n) cta_copy<ES>(x + tb, dst_shard, len);
       int ro = 0;
       for (int r = 0; r < n; r++) {
@@ -699,7 +707,7 @@ struct AgOp {
         PtrList dst;
         dst.add(y + (size_t)r * R + tb + pj0);
         for (int i = 0; i < d; i++)
-          if (i != j) dst.add(slot_ptr<T>(a, peer(i), ch, slot) + (size_t)j * RG + TL + (size_t)ro * Pc);
+          if (i != j) dst.add(slot_ptr<T>(a, peer(i), ch, slot) + (size_t)cidx(j, i) * RG + TL + (size_t)ro * Pc);
         cta_copy<ES>(xin + (size_t)ro * Pc, dst, pj1 - pj0);
         ro++;
       }
@@ -707,7 +715,7 @@ struct AgOp {
       for (int i = 0; i < d; i++) {
         if (i == j) continue;
         const int pr = peer(i);
-        const T* reg = mine + (size_t)i * RG;
+        const T* reg = mine + (size_t)cidx(i, j) * RG;
         cta_copy1<ES>(reg, y + (size_t)pr * R + tb, len);
         const size_t pi0 = sub_lo(len, TL, d, i), pi1 = sub_lo(len, TL, d, i + 1);
         int ro = 0;
@@ -723,7 +731,7 @@ struct AgOp {
 
 // ================================================================== Broadcast (a8) =============
 // Root -> its domain members (scatter of regions) -> one owner per other domain per segment ->
-// intra-domain all-gather. Slot layout on a rank of domain k (Rk = T/d): reg[Rk] | s3[d][Rk]
+// intra-domain all-gather. Slot layout on a rank of domain k (Rk = T/d): reg[Rk] | s3[d-1][Rk]
 // Stages: 0 A root scatter | 1 B cross push | 2 C region -> y and domain peers | 3 D peers -> y
 template <typename T>
 struct BcOp {
@@ -788,7 +796,7 @@ struct BcOp {
         if (i == j) continue;
         const int pr = peer(i);
         if (pr == root) continue;
-        dst.add(slot_ptr<T>(a, pr, ch, slot) + Rk + (size_t)j * Rk);
+        dst.add(slot_ptr<T>(a, pr, ch, slot) + Rk + (size_t)cidx(j, i) * Rk);
       }
       if (dst.n) cta_copy<ES>(myreg, dst, r1 - r0);
       if (is_root && x != y) cta_copy1<ES>(x + tb, y + tb, len);
@@ -797,7 +805,7 @@ struct BcOp {
       for (int i = 0; i < d; i++) {
         if (i == j) continue;
         const size_t p0 = g.seg(i * spj), p1 = g.seg((i + 1) * spj);
-        cta_copy1<ES>(mine + Rk + (size_t)i * Rk, y + tb + p0, p1 - p0);
+        cta_copy1<ES>(mine + Rk + (size_t)cidx(i, j) * Rk, y + tb + p0, p1 - p0);
       }
     }
   }

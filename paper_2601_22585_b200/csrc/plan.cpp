@@ -60,22 +60,43 @@ static size_t quantum(const Topo& t, int op, int V) {
 }
 
 size_t slot_mult_num(const Topo& t, int op, size_t tile) {
-  size_t dmin = (size_t)t.dmin, n = (size_t)t.n, D = (size_t)t.D;
-  switch (op) {
-    case OP_ALLREDUCE:  // s1[d][T/d] + s2[D][T/d] + ag[T/d] + s3[d][T/d]
-      return 2 * tile + (D + 1) * (tile / dmin);
-    case OP_REDUCE_SCATTER:  // s1[d][T + (n-d)T/d] + s2[D][T]
-      return n * tile + D * tile;
-    case OP_ALL_GATHER:  // s_in[d][T + (n-d)T/d] + xin[(n-d)T/d]
-      return n * tile + (n - dmin) * (tile / dmin);
-    case OP_BROADCAST:  // reg[T/d] + s3[d][T/d]
-      return tile + tile / dmin;
-    default:
-      return 0;
+  // the largest per-rank slot layout over the domains (kernels.cu; s1/s3 hold domain PEERS only)
+  const size_t n = (size_t)t.n, D = (size_t)t.D;
+  size_t need = 0;
+  for (int k = 0; k < t.D; k++) {
+    const size_t d = (size_t)t.dom_size[k], Rk = tile / d, RG = tile + (n - d) * Rk;
+    size_t v = 0;
+    switch (op) {
+      case OP_ALLREDUCE:  // s1[d-1][Rk] | s2[D][Rk] | ag[Rk] | s3[d-1][Rk]
+        v = (2 * (d - 1) + D + 1) * Rk;
+        break;
+      case OP_REDUCE_SCATTER:  // s1[d-1][RG] | s2[D][T]
+        v = (d - 1) * RG + D * tile;
+        break;
+      case OP_ALL_GATHER:  // s_in[d-1][RG] | xin[n-d][T/d]
+        v = (d - 1) * RG + (n - d) * Rk;
+        break;
+      case OP_BROADCAST:  // reg[Rk] | s3[d-1][Rk]
+        v = d * Rk;
+        break;
+    }
+    need = std::max(need, v);
   }
+  return need;
 }
 
-static size_t default_tile_bytes(int op, int n) {
+// default scratch slot (bytes) for a topology: fits the default tile of every op
+size_t default_slot_bytes(const Topo& t, size_t tile_bytes) {
+  size_t need = 0;
+  for (int op = OP_ALLREDUCE; op <= OP_BROADCAST; op++) {
+    size_t tb = tile_bytes;
+    if (op == OP_REDUCE_SCATTER || op == OP_ALL_GATHER) tb = std::max<size_t>(tile_bytes / (size_t)t.n, 4096);
+    need = std::max(need, slot_mult_num(t, op, tb));
+  }
+  return (need + 4095) / 4096 * 4096 + 65536;  // room for the quantum rounding of the tile
+}
+
+size_t default_tile_bytes(int op, int n) {
   const char* e = getenv("HETCCL_TILE_KB");
   size_t b = e ? (size_t)atol(e) * 1024 : (size_t)256 * 1024;
   if (op == OP_REDUCE_SCATTER || op == OP_ALL_GATHER) b /= (size_t)n;  // RS/AG tiles are per shard

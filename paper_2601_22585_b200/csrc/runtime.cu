@@ -85,7 +85,10 @@ long env_long(const char* name, long dflt) {
 
 void read_env(hetcclComm* c) {
   c->nch_max = (int)std::max(1L, std::min((long)kMaxChannels, env_long("HETCCL_NCHANNELS", 128)));
-  c->slot_bytes = (size_t)std::max(64L, env_long("HETCCL_SLOT_KB", 768)) * 1024;
+  // scratch slot: HETCCL_SLOT_KB, else sized from this map so every op's default tile fits
+  const long slot_kb = env_long("HETCCL_SLOT_KB", 0);
+  c->slot_bytes = slot_kb > 0 ? (size_t)std::max(64L, slot_kb) * 1024
+                              : default_slot_bytes(c->topo, default_tile_bytes(OP_ALLREDUCE, c->topo.n));
   c->slot_bytes = (c->slot_bytes + 255) / 256 * 256;
   c->timeout_ns = (long long)std::max(1L, env_long("HETCCL_TIMEOUT_S", 30)) * 1000000000LL;
   c->trace_iters = (int)std::max(0L, std::min(4096L, env_long("HETCCL_TRACE_ITERS", 0)));
@@ -381,6 +384,12 @@ hetcclResult_t hetccl_comm_init_mux(hetcclComm_t* comm, int nranks, const int* r
   c->kind = KIND_MUX;
   c->device = cuda_device;
   DevGuard g(cuda_device);
+  {  // all ranks' CTAs must be co-resident (one per SM): channels per rank <= SMs / nranks
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cuda_device);
+    c->nch_max = std::max(1, std::min(c->nch_max, sms / nranks));
+    c->alloc_bytes = kFlagsReserve + (size_t)c->nch_max * kNumSlots * c->slot_bytes;
+  }
   cudaError_t e = cudaSuccess;
   for (int r = 0; r < nranks && e == cudaSuccess; r++) e = alloc_region(c->alloc_bytes, &c->local[r]);
   if (e == cudaSuccess) e = cudaMalloc((void**)&c->err, 8);
@@ -504,6 +513,7 @@ hetcclResult_t hetccl_plan_info(int nranks, const int* rank_to_domain, int rank,
       !valid_dt(dt) || (op == OP_BROADCAST && (root < 0 || root >= nranks)))
     return hetcclInvalidArgument;
   hetcclComm tmp;
+  tmp.topo = t;
   read_env(&tmp);
   const int es = dtype_size(dt);
   const int nch = nchannels > 0 ? std::min(nchannels, kMaxChannels) : tmp.nch_max;
@@ -549,6 +559,7 @@ hetcclResult_t hetccl_comm_get_trace(hetcclComm_t c, void* host, size_t bytes, i
     shape[0] = shape[1] = shape[2] = 0;
     return hetcclSuccess;
   }
+  if (!host) return hetcclSuccess;  // shape query
   if (!host || bytes < need) return fail(c, hetcclInvalidArgument, "trace buffer needs %zu bytes", need);
   DevGuard g(c->device);
   CUDA_TRY(c, cudaDeviceSynchronize());

@@ -112,3 +112,24 @@ def test_n1_copy():
         assert torch.equal(x, y)
     finally:
         hc.hetccl_comm_destroy(comm)
+
+
+def test_trace_stamps_monotone(monkeypatch):
+    """HETCCL_TRACE_ITERS: per-iteration stamps are ordered wait <= work <= end <= fenced."""
+    import torch
+    monkeypatch.setenv("HETCCL_TRACE_ITERS", "16")
+    hc = _hc()
+    m = MAPS["2+2"]
+    comm = hc.hetccl_comm_init_mux(4, m, 0)
+    try:
+        xs = [torch.randn(1 << 20, device="cuda") for _ in range(4)]
+        ys = [torch.empty_like(x) for x in xs]
+        hc.mux_allreduce(xs, ys, comm)
+        tr = hc.hetccl_comm_get_trace(comm)
+        assert tr is not None and tr.shape[0] == 4 and tr.shape[3] == 4
+        used = tr[..., 0] > 0
+        assert used.any()
+        for k in range(3):
+            assert np.all(tr[..., k + 1][used] >= tr[..., k][used])
+    finally:
+        hc.hetccl_comm_destroy(comm)
