@@ -20,7 +20,7 @@ namespace hetccl {
 
 constexpr int kMaxRanks = 16;      // == HETCCL_MAX_RANKS (one flag line = 16 senders x 8 B)
 constexpr int kMaxChannels = 148;  // hard cap on CTAs per rank per op (one per SM)
-constexpr int kNumSlots = 8;       // scratch ring depth per channel (> pipeline depth)
+constexpr int kNumSlots = 12;      // scratch ring depth per channel (> pipeline depth 2*5-1 + 1)
 constexpr int kThreads = 512;      // threads per CTA
 constexpr int kMaxStages = 5;      // pipeline positions of the deepest op (All-Reduce)
 
@@ -90,6 +90,7 @@ struct OpArgs {
   long long timeout_ns;
   unsigned long long* trace;    // optional per-iteration timestamps (HETCCL_TRACE_ITERS), else null
   int trace_iters;
+  int ws;                       // 1: warp-specialised pipeline (HETCCL_WS, default), 0: plain
 };
 
 // ---- host plan (plan.cpp) ----

@@ -168,6 +168,10 @@ __device__ __forceinline__ bool all_aligned16(const PtrList& a, const PtrList& b
   return (o & 15) == 0;
 }
 
+// data-thread geometry of the current CTA (set by run_pipeline: warp-specialised CTAs leave warp 0
+// to the flag protocol), read by the data movers
+__shared__ int g_dbase, g_dnth;
+
 constexpr int kUnroll = 4;      // vectors in flight per thread per source in a fold
 constexpr int kCopyUnroll = 8;  // vectors in flight per thread in a copy
 
@@ -176,7 +180,7 @@ template <int ES>
 __device__ __noinline__ void cta_copy(const void* src, const PtrList& dsts, size_t n) {
   if (n == 0) return;
   constexpr int V = 16 / ES;
-  const int tid = threadIdx.x, nth = blockDim.x;
+  const int tid = (int)threadIdx.x - g_dbase, nth = g_dnth;
   PtrList s1;
   s1.add(src);
   const size_t nv = all_aligned16(s1, dsts) ? n / V : 0;
@@ -227,7 +231,7 @@ __device__ __noinline__ void cta_fold(const PtrList& srcs, const PtrList& dsts, 
     cta_copy<sizeof(S)>(srcs.p[0], dsts, n);
     return;
   }
-  const int tid = threadIdx.x, nth = blockDim.x;
+  const int tid = (int)threadIdx.x - g_dbase, nth = g_dnth;
   const size_t nv = all_aligned16(srcs, dsts) ? n / V : 0;
   for (size_t v0 = tid; v0 < nv; v0 += (size_t)kUnroll * nth) {
     A acc[kUnroll][V];
@@ -325,18 +329,23 @@ __device__ __forceinline__ int owner_of(const Topo& t, int q, int s) {
 
 // ================================================================== pipeline driver ===========
 // Software pipeline over the tiles t = ch, ch + nch, ... of one channel. The op's active logical
-// stages occupy positions 0..np-1 (identical on every rank); iteration `it` runs the stage at
-// position p on the channel's local tile it - p. Per iteration:
-//   1. warp 0, lane p polls sender p's counters: for every stage due this iteration, its wait
-//      counter must show the tile (cumulative target base + tile + 1); position 0 also waits for
-//      the ACK of the tile that last used the slot (slot reuse, kNumSlots deep ring);
-//   2. __syncthreads; every stage due runs on its tile (all 512 threads, 16-byte vectors);
-//   3. __syncthreads; warp 0 executes fence.acq_rel.sys (all data of the iteration, local and
-//      remote, is performed at system scope), then lane r adds 1 to rank r's counter for every
-//      stage that signals r; after the last position's tile, every other rank gets an ACK.
-// A producer stage always sits at an earlier position than its consumer and kNumSlots exceeds the
-// pipeline depth, so every wait of iteration it depends only on iterations < it of other ranks:
-// no cycle, hence no deadlock with all CTAs co-resident.
+// stages occupy positions 0, SP, 2*SP, ... (identical on every rank); iteration `it` runs the stage at
+// position p on the channel's local tile it - p. Warp 0 is the SYNC warp (polls, fences, signals);
+// in the default warp-specialised mode (SP = 2) warps 1..15 move data while warp 0 releases the
+// previous iteration, so the release fence (which waits for every outstanding NVLink store to be
+// acknowledged) never stalls the data warps:
+//   sync warp:  poll(0); for it: GO | fence; signal(it-1) | DONE | poll(it+1);  fence; signal(last)
+//   data warps:          for it: GO | work(it)             | DONE
+//   poll(it):   lane p polls sender p's counter of every stage due in iteration it (cumulative
+//               target base + tile + 1) and, for position 0, the ACK of the tile that last used
+//               the slot (kNumSlots-deep ring);
+//   signal(it): lane r adds 1 to rank r's counter for every stage of iteration it that signals r,
+//               and after the last position's tile an ACK to every other rank.
+// Because signal(it) is only sent during iteration it+1, a consumer sits SP = 2 positions after its
+// producer: poll(it) then needs other ranks' signals of iterations <= it-2, sent in their window
+// it-1, which needs their poll(it-1) — by induction no cycle, hence no deadlock with all CTAs
+// co-resident. (HETCCL_WS=0 selects the plain mode: SP = 1, all 16 warps move data, and the sync
+// warp fences and signals iteration it before polling it+1.)
 struct PipeShared {
   unsigned long long base[kCounters][kMaxRanks];
   unsigned long long tiles0;
@@ -344,95 +353,164 @@ struct PipeShared {
 };
 
 template <class Op>
-__device__ __forceinline__ void run_pipeline(const OpArgs& a, Op& op, int me, int ch) {
-  __shared__ PipeShared ps;
-  const RankPlan& rp = a.rp[me];
-  const int n = a.topo.n;
-  uint64_t* F = chan_flags(a, me, ch);
-  uint64_t* B = chan_base(a, me, ch);
-  int stage_at[kMaxStages];
-  int np = 0;
-#pragma unroll
-  for (int s = 0; s < kMaxStages; s++)
-    if ((a.active >> s) & 1u) stage_at[np++] = s;
-  if (threadIdx.x < kCounters * kMaxRanks) ps.base[threadIdx.x / kMaxRanks][threadIdx.x % kMaxRanks] = B[threadIdx.x / kMaxRanks * kLineWords + threadIdx.x % kMaxRanks];
-  if (threadIdx.x == 0) {
-    ps.tiles0 = B[kCounters * kLineWords];
-    ps.abort_ = 0;
+struct Pipe {
+  const OpArgs& a;
+  Op& op;
+  PipeShared& ps;
+  const RankPlan& rp;
+  int me, ch, n, np, SP, npos, lane;
+  long long ntl;
+  unsigned long long tiles0;
+  int stage_at[2 * kMaxStages];  // logical stage at each position, -1 for a bubble
+  uint64_t* F;
+
+  __device__ bool tile_at(long long it, int p, long long& tl) const {
+    tl = it - p;
+    return tl >= 0 && tl < ntl;
   }
-  __syncthreads();
-  const long long ntl = (ch < (long long)a.ntiles) ? ((long long)a.ntiles - ch + a.nch - 1) / a.nch : 0;
-  const unsigned long long tiles0 = ps.tiles0;
-  const int lane = threadIdx.x & 31;
-  unsigned long long* trc = nullptr;  // [it][4] globaltimer stamps: wait start, work start, work end, fenced
-  if (a.trace) trc = a.trace + ((size_t)blockIdx.y * gridDim.x + ch) * (size_t)a.trace_iters * 4;
-  for (long long it = 0; it < ntl + np - 1; ++it) {
-    const bool tr = trc && threadIdx.x == 0 && it < a.trace_iters;
-    if (tr) trc[it * 4 + 0] = globaltimer();
-    // ---- 1. waits (warp 0; lane = sender) ----
-    if (threadIdx.x < 32) {
-      bool ok = true;
-      if (lane < n) {
-        for (int p = 0; p < np && ok; p++) {
-          const long long tl = it - p;
-          if (tl < 0 || tl >= ntl) continue;
-          const int s = stage_at[p];
-          const uint64_t* w1 = nullptr;
-          uint64_t t1 = 0;
-          if (p == 0 && ((rp.writes >> lane) & 1u) && tiles0 + tl >= (unsigned long long)kNumSlots) {
-            w1 = F + C_ACK * kLineWords + lane;
-            t1 = tiles0 + tl - kNumSlots + 1;
-          }
-          const int wc = rp.wait_ctr[s];
-          const uint64_t* w2 = nullptr;
-          uint64_t t2 = 0;
-          if (wc != C_NONE && ((rp.wait_mask[s] >> lane) & 1u)) {
-            w2 = F + wc * kLineWords + lane;
-            t2 = ps.base[wc][lane] + tl + 1;
-          }
-          for (int q = 0; q < 2 && ok; q++) {
-            const uint64_t* w = q ? w2 : w1;
-            const uint64_t tg = q ? t2 : t1;
-            if (!w || ld_acquire_sys(w) >= tg) continue;
-            const uint64_t t0 = globaltimer();
-            uint32_t spins = 0;
-            while (ld_acquire_sys(w) < tg) {
-              if ((++spins & 1023u) == 0 && (long long)(globaltimer() - t0) > a.timeout_ns) {
-                atomicOr(a.err, 1ull + ((unsigned long long)(q ? wc : C_ACK) << 8) + ((unsigned long long)lane << 16));
-                ok = false;
-                break;
-              }
-            }
+  // sync warp: wait for everything iteration `it` needs; false on timeout
+  __device__ bool poll(long long it) {
+    bool ok = true;
+    if (lane >= n) return true;
+    for (int p = 0; p < npos && ok; p++) {
+      long long tl;
+      if (stage_at[p] < 0 || !tile_at(it, p, tl)) continue;
+      const int s = stage_at[p];
+      const uint64_t* w1 = nullptr;
+      uint64_t t1 = 0;
+      if (p == 0 && ((rp.writes >> lane) & 1u) && tiles0 + tl >= (unsigned long long)kNumSlots) {
+        w1 = F + C_ACK * kLineWords + lane;
+        t1 = tiles0 + tl - kNumSlots + 1;
+      }
+      const int wc = rp.wait_ctr[s];
+      const uint64_t* w2 = nullptr;
+      uint64_t t2 = 0;
+      if (wc != C_NONE && ((rp.wait_mask[s] >> lane) & 1u)) {
+        w2 = F + wc * kLineWords + lane;
+        t2 = ps.base[wc][lane] + tl + 1;
+      }
+      for (int q = 0; q < 2 && ok; q++) {
+        const uint64_t* w = q ? w2 : w1;
+        const uint64_t tg = q ? t2 : t1;
+        if (!w || ld_acquire_sys(w) >= tg) continue;
+        const uint64_t t0 = globaltimer();
+        uint32_t spins = 0;
+        while (ld_acquire_sys(w) < tg) {
+          if ((++spins & 1023u) == 0 && (long long)(globaltimer() - t0) > a.timeout_ns) {
+            atomicOr(a.err, 1ull + ((unsigned long long)(q ? wc : C_ACK) << 8) + ((unsigned long long)lane << 16));
+            ok = false;
+            break;
           }
         }
       }
-      if (!ok) ps.abort_ = 1;
     }
-    __syncthreads();
-    if (*(volatile int*)&ps.abort_) break;
-    if (tr) trc[it * 4 + 1] = globaltimer();
-    // ---- 2. stage work ----
-    for (int p = 0; p < np; p++) {
-      const long long tl = it - p;
-      if (tl < 0 || tl >= ntl) continue;
+    return ok;
+  }
+  // sync warp: every data store of iteration `it` is complete (caller fenced); signal its receivers
+  __device__ void signal(long long it) {
+    if (lane >= n || lane == me) return;
+    int last = -1;
+    for (int p = 0; p < npos; p++) {
+      long long tl;
+      if (stage_at[p] < 0) continue;
+      last = p;
+      if (!tile_at(it, p, tl)) continue;
+      const int s = stage_at[p];
+      if (rp.sig_ctr[s] != C_NONE && ((rp.sig_mask[s] >> lane) & 1u))
+        red_add_relaxed_sys(chan_flags(a, lane, ch) + rp.sig_ctr[s] * kLineWords + me, 1);
+    }
+    long long tl;
+    if (last >= 0 && tile_at(it, last, tl)) red_add_relaxed_sys(chan_flags(a, lane, ch) + C_ACK * kLineWords + me, 1);
+  }
+  __device__ void work(long long it) {
+    for (int p = 0; p < npos; p++) {
+      long long tl;
+      if (stage_at[p] < 0 || !tile_at(it, p, tl)) continue;
       op.stage(stage_at[p], (size_t)ch + (size_t)tl * a.nch, (int)((tiles0 + tl) % kNumSlots));
     }
-    __syncthreads();
-    if (tr) trc[it * 4 + 2] = globaltimer();
-    // ---- 3. release: fence, then signals ----
-    if (threadIdx.x < 32) {
-      fence_acq_rel_sys();
-      if (tr) trc[it * 4 + 3] = globaltimer();
-      if (lane < n && lane != me) {
-        for (int p = 0; p < np; p++) {
-          const long long tl = it - p;
-          if (tl < 0 || tl >= ntl) continue;
-          const int s = stage_at[p];
-          if (rp.sig_ctr[s] != C_NONE && ((rp.sig_mask[s] >> lane) & 1u))
-            red_add_relaxed_sys(chan_flags(a, lane, ch) + rp.sig_ctr[s] * kLineWords + me, 1);
+  }
+};
+
+template <class Op>
+__device__ __forceinline__ void run_pipeline(const OpArgs& a, Op& op, int me, int ch) {
+  __shared__ PipeShared ps;
+  Pipe<Op> P{a, op, ps, a.rp[me]};
+  P.me = me;
+  P.ch = ch;
+  P.n = a.topo.n;
+  P.lane = threadIdx.x & 31;
+  P.F = chan_flags(a, me, ch);
+  uint64_t* B = chan_base(a, me, ch);
+  const bool ws = a.ws != 0;
+  P.SP = ws ? 2 : 1;
+  P.np = 0;
+  for (int p = 0; p < 2 * kMaxStages; p++) P.stage_at[p] = -1;
+#pragma unroll
+  for (int s = 0; s < kMaxStages; s++)
+    if ((a.active >> s) & 1u) P.stage_at[P.SP * P.np++] = s;
+  P.npos = P.SP * (P.np - 1) + 1;
+  if (threadIdx.x < kCounters * kMaxRanks)
+    ps.base[threadIdx.x / kMaxRanks][threadIdx.x % kMaxRanks] = B[threadIdx.x / kMaxRanks * kLineWords + threadIdx.x % kMaxRanks];
+  if (threadIdx.x == 0) {
+    ps.tiles0 = B[kCounters * kLineWords];
+    ps.abort_ = 0;
+    g_dbase = ws ? 32 : 0;
+    g_dnth = ws ? (int)blockDim.x - 32 : (int)blockDim.x;
+  }
+  __syncthreads();
+  P.ntl = (ch < (long long)a.ntiles) ? ((long long)a.ntiles - ch + a.nch - 1) / a.nch : 0;
+  P.tiles0 = ps.tiles0;
+  const long long nit = P.ntl > 0 ? P.ntl + P.npos - 1 : 0;
+  const bool sync_warp = threadIdx.x < 32;
+  unsigned long long* trc = nullptr;  // [it][4] globaltimer stamps: poll start, GO, DONE, fenced
+  if (a.trace) trc = a.trace + ((size_t)blockIdx.y * gridDim.x + ch) * (size_t)a.trace_iters * 4;
+  auto stamp = [&](long long it, int k) {
+    if (trc && threadIdx.x == 0 && it >= 0 && it < a.trace_iters) trc[it * 4 + k] = globaltimer();
+  };
+  if (ws) {
+    if (sync_warp && nit > 0) {
+      stamp(0, 0);
+      if (!P.poll(0)) ps.abort_ = 1;
+    }
+    for (long long it = 0; it < nit; ++it) {
+      __syncthreads();  // GO(it)
+      if (*(volatile int*)&ps.abort_) break;
+      stamp(it, 1);
+      if (sync_warp) {
+        if (it > 0) {
+          fence_acq_rel_sys();
+          stamp(it - 1, 3);
+          P.signal(it - 1);
         }
-        const long long tl = it - (np - 1);
-        if (tl >= 0 && tl < ntl) red_add_relaxed_sys(chan_flags(a, lane, ch) + C_ACK * kLineWords + me, 1);
+      } else {
+        P.work(it);
+      }
+      __syncthreads();  // DONE(it)
+      stamp(it, 2);
+      if (sync_warp && it + 1 < nit) {
+        stamp(it + 1, 0);
+        if (!P.poll(it + 1)) ps.abort_ = 1;
+      }
+    }
+    if (sync_warp && nit > 0 && !*(volatile int*)&ps.abort_) {
+      fence_acq_rel_sys();
+      stamp(nit - 1, 3);
+      P.signal(nit - 1);
+    }
+  } else {
+    for (long long it = 0; it < nit; ++it) {
+      stamp(it, 0);
+      if (sync_warp && !P.poll(it)) ps.abort_ = 1;
+      __syncthreads();
+      if (*(volatile int*)&ps.abort_) break;
+      stamp(it, 1);
+      P.work(it);
+      __syncthreads();
+      stamp(it, 2);
+      if (sync_warp) {
+        fence_acq_rel_sys();
+        stamp(it, 3);
+        P.signal(it);
       }
     }
   }
@@ -440,12 +518,13 @@ __device__ __forceinline__ void run_pipeline(const OpArgs& a, Op& op, int me, in
   // ---- exit: advance this rank's cumulative targets by the tiles this launch processed ----
   if (!ps.abort_ && threadIdx.x < kMaxRanks) {
     const int p = threadIdx.x;
+    const RankPlan& rp = a.rp[me];
     for (int s = 0; s < kMaxStages; s++) {
       if (!((a.active >> s) & 1u)) continue;
       const int wc = rp.wait_ctr[s];
-      if (wc != C_NONE && ((rp.wait_mask[s] >> p) & 1u)) B[wc * kLineWords + p] = ps.base[wc][p] + ntl;
+      if (wc != C_NONE && ((rp.wait_mask[s] >> p) & 1u)) B[wc * kLineWords + p] = ps.base[wc][p] + P.ntl;
     }
-    if (p == 0) B[kCounters * kLineWords] = tiles0 + ntl;
+    if (p == 0) B[kCounters * kLineWords] = P.tiles0 + P.ntl;
   }
 }
 

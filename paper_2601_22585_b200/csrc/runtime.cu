@@ -39,6 +39,7 @@ struct hetcclComm {
   bool connected = false;
   long long timeout_ns = 30LL * 1000000000LL;
   int trace_iters = 0;                    // HETCCL_TRACE_ITERS: per-iteration timestamps of the last op
+  int ws = 1;                             // HETCCL_WS: warp-specialised pipeline
   unsigned long long* trace = nullptr;
   size_t trace_bytes = 0;
   int trace_shape[2] = {0, 0};            // local ranks, channels of the last traced op
@@ -92,6 +93,7 @@ void read_env(hetcclComm* c) {
   c->slot_bytes = (c->slot_bytes + 255) / 256 * 256;
   c->timeout_ns = (long long)std::max(1L, env_long("HETCCL_TIMEOUT_S", 30)) * 1000000000LL;
   c->trace_iters = (int)std::max(0L, std::min(4096L, env_long("HETCCL_TRACE_ITERS", 0)));
+  c->ws = env_long("HETCCL_WS", 1) != 0;
   c->alloc_bytes = kFlagsReserve + (size_t)c->nch_max * kNumSlots * c->slot_bytes;
 }
 
@@ -202,6 +204,7 @@ hetcclResult_t run_op(hetcclComm_t c, int op, const void* const* sends, void* co
   a.active = active_stages(c->topo, op, root);
   a.err = c->err;
   a.timeout_ns = c->timeout_ns;
+  a.ws = c->ws;
   if (c->trace_iters > 0) {
     const size_t need = (size_t)nlocal * geo.nch * c->trace_iters * 4 * sizeof(unsigned long long);
     if (need > c->trace_bytes) {
