@@ -10,7 +10,7 @@
 //             sender), advanced by each launch at exit, plus the channel's cumulative tile count in
 //             word 0 of counter line kCounters. Targets are cumulative across launches, so the
 //             protocol needs no host sequence numbers and survives CUDA-graph replay.
-//   scratch : [channel][slot] ring of kNumSlots slots of slot_elems elements; slot g % kNumSlots
+//   scratch : [channel][slot] ring of nslots (<= kMaxSlots) slots of slot_elems elements; slot g % nslots
 //             holds every staging buffer cumulative tile g of that channel needs on this rank.
 #pragma once
 #include <stddef.h>
@@ -20,7 +20,7 @@ namespace hetccl {
 
 constexpr int kMaxRanks = 16;      // == HETCCL_MAX_RANKS (one flag line = 16 senders x 8 B)
 constexpr int kMaxChannels = 148;  // hard cap on CTAs per rank per op (one per SM)
-constexpr int kNumSlots = 12;      // scratch ring depth per channel (> pipeline depth 2*5-1 + 1)
+constexpr int kMaxSlots = 16;      // cap on the scratch ring depth per channel (HETCCL_NSLOTS)
 constexpr int kThreads = 512;      // threads per CTA
 constexpr int kMaxStages = 5;      // pipeline positions of the deepest op (All-Reduce)
 
@@ -90,7 +90,8 @@ struct OpArgs {
   long long timeout_ns;
   unsigned long long* trace;    // optional per-iteration timestamps (HETCCL_TRACE_ITERS), else null
   int trace_iters;
-  int ws;                       // 1: warp-specialised pipeline (HETCCL_WS, default), 0: plain
+  int ws;                       // 0: plain pipeline; k >= 2: warp-specialised, consumers k positions after producers
+  int nslots;                   // scratch ring depth (> pipeline positions)
 };
 
 // ---- host plan (plan.cpp) ----

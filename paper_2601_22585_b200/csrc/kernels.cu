@@ -12,7 +12,7 @@
 //           receiver's counter word of this sender;
 //   reader: lane p of warp 0 spins ld.acquire.sys on sender p's word until it reaches the
 //           cumulative target -> __syncthreads -> ld.global.cg of the staged data.
-// Scratch is a ring of kNumSlots slots per channel indexed by the channel's cumulative tile count;
+// Scratch is a ring of nslots slots per channel indexed by the channel's cumulative tile count;
 // before writing a tile's slot a rank waits for the ACK of the tile that last used it. Targets are
 // cumulative across launches (kept in the rank's own base lines), so the protocol needs no host
 // sequence numbers and replays under CUDA graphs. The same kernels serve the rank-multiplexed mode
@@ -301,7 +301,7 @@ __device__ __forceinline__ uint64_t* chan_base(const OpArgs& a, int rank, int ch
 
 template <typename T>
 __device__ __forceinline__ T* slot_ptr(const OpArgs& a, int rank, int ch, int slot) {
-  return (T*)(a.mem[rank].scratch + ((size_t)(ch * kNumSlots + slot) * a.slot_elems) * sizeof(T));
+  return (T*)(a.mem[rank].scratch + ((size_t)ch * a.nslots + slot) * a.slot_elems * sizeof(T));
 }
 
 __device__ __forceinline__ size_t floor_to(size_t x, size_t q) { return x / q * q; }
@@ -338,7 +338,7 @@ __device__ __forceinline__ int owner_of(const Topo& t, int q, int s) {
 //   data warps:          for it: GO | work(it)             | DONE
 //   poll(it):   lane p polls sender p's counter of every stage due in iteration it (cumulative
 //               target base + tile + 1) and, for position 0, the ACK of the tile that last used
-//               the slot (kNumSlots-deep ring);
+//               the slot (nslots-deep ring);
 //   signal(it): lane r adds 1 to rank r's counter for every stage of iteration it that signals r,
 //               and after the last position's tile an ACK to every other rank.
 // Because signal(it) is only sent during iteration it+1, a consumer sits SP = 2 positions after its
@@ -361,7 +361,7 @@ struct Pipe {
   int me, ch, n, np, SP, npos, lane;
   long long ntl;
   unsigned long long tiles0;
-  int stage_at[2 * kMaxStages];  // logical stage at each position, -1 for a bubble
+  int stage_at[4 * kMaxStages];  // logical stage at each position, -1 for a bubble
   uint64_t* F;
 
   __device__ bool tile_at(long long it, int p, long long& tl) const {
@@ -378,9 +378,9 @@ struct Pipe {
       const int s = stage_at[p];
       const uint64_t* w1 = nullptr;
       uint64_t t1 = 0;
-      if (p == 0 && ((rp.writes >> lane) & 1u) && tiles0 + tl >= (unsigned long long)kNumSlots) {
+      if (p == 0 && ((rp.writes >> lane) & 1u) && tiles0 + tl >= (unsigned long long)a.nslots) {
         w1 = F + C_ACK * kLineWords + lane;
-        t1 = tiles0 + tl - kNumSlots + 1;
+        t1 = tiles0 + tl - a.nslots + 1;
       }
       const int wc = rp.wait_ctr[s];
       const uint64_t* w2 = nullptr;
@@ -426,7 +426,7 @@ struct Pipe {
     for (int p = 0; p < npos; p++) {
       long long tl;
       if (stage_at[p] < 0 || !tile_at(it, p, tl)) continue;
-      op.stage(stage_at[p], (size_t)ch + (size_t)tl * a.nch, (int)((tiles0 + tl) % kNumSlots));
+      op.stage(stage_at[p], (size_t)ch + (size_t)tl * a.nch, (int)((tiles0 + tl) % (unsigned long long)a.nslots));
     }
   }
 };
@@ -441,10 +441,10 @@ __device__ __forceinline__ void run_pipeline(const OpArgs& a, Op& op, int me, in
   P.lane = threadIdx.x & 31;
   P.F = chan_flags(a, me, ch);
   uint64_t* B = chan_base(a, me, ch);
-  const bool ws = a.ws != 0;
-  P.SP = ws ? 2 : 1;
+  const bool ws = a.ws >= 2;
+  P.SP = ws ? a.ws : 1;
   P.np = 0;
-  for (int p = 0; p < 2 * kMaxStages; p++) P.stage_at[p] = -1;
+  for (int p = 0; p < 4 * kMaxStages; p++) P.stage_at[p] = -1;
 #pragma unroll
   for (int s = 0; s < kMaxStages; s++)
     if ((a.active >> s) & 1u) P.stage_at[P.SP * P.np++] = s;

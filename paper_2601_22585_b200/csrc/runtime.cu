@@ -39,7 +39,8 @@ struct hetcclComm {
   bool connected = false;
   long long timeout_ns = 30LL * 1000000000LL;
   int trace_iters = 0;                    // HETCCL_TRACE_ITERS: per-iteration timestamps of the last op
-  int ws = 1;                             // HETCCL_WS: warp-specialised pipeline
+  int ws = 0;                             // HETCCL_WS: 0 plain pipeline, k in 2..4 warp-specialised (spacing k)
+  int nslots = 8;                         // HETCCL_NSLOTS: scratch ring depth
   unsigned long long* trace = nullptr;
   size_t trace_bytes = 0;
   int trace_shape[2] = {0, 0};            // local ranks, channels of the last traced op
@@ -55,6 +56,8 @@ struct Blob {
   int map[kMaxRanks];
   unsigned long long slot_bytes;
   int nch_max;
+  int ws;
+  int nslots;
   int pad;
   cudaIpcMemHandle_t handle;
 };
@@ -93,8 +96,11 @@ void read_env(hetcclComm* c) {
   c->slot_bytes = (c->slot_bytes + 255) / 256 * 256;
   c->timeout_ns = (long long)std::max(1L, env_long("HETCCL_TIMEOUT_S", 30)) * 1000000000LL;
   c->trace_iters = (int)std::max(0L, std::min(4096L, env_long("HETCCL_TRACE_ITERS", 0)));
-  c->ws = env_long("HETCCL_WS", 1) != 0;
-  c->alloc_bytes = kFlagsReserve + (size_t)c->nch_max * kNumSlots * c->slot_bytes;
+  c->ws = (int)env_long("HETCCL_WS", 0);
+  if (c->ws == 1 || c->ws < 0) c->ws = 0;
+  if (c->ws > 4) c->ws = 4;
+  c->nslots = (int)std::max(2L, std::min((long)kMaxSlots, env_long("HETCCL_NSLOTS", 8)));
+  c->alloc_bytes = kFlagsReserve + (size_t)c->nch_max * c->nslots * c->slot_bytes;
 }
 
 // allocate one rank's [flags | scratch] region on the current device, flags zeroed
@@ -205,6 +211,14 @@ hetcclResult_t run_op(hetcclComm_t c, int op, const void* const* sends, void* co
   a.err = c->err;
   a.timeout_ns = c->timeout_ns;
   a.ws = c->ws;
+  a.nslots = c->nslots;
+  {  // the ring must be deeper than the pipeline (plus the one-iteration release lag of the WS mode)
+    int na = 0;
+    for (int s = 0; s < kMaxStages; s++) na += (a.active >> s) & 1;
+    const int npos = (c->ws >= 2 ? c->ws : 1) * (na - 1) + 1 + (c->ws >= 2 ? 1 : 0);
+    if (c->nslots <= npos)
+      return fail(c, hetcclInvalidUsage, "HETCCL_NSLOTS=%d must exceed the pipeline depth %d", c->nslots, npos);
+  }
   if (c->trace_iters > 0) {
     const size_t need = (size_t)nlocal * geo.nch * c->trace_iters * 4 * sizeof(unsigned long long);
     if (need > c->trace_bytes) {
@@ -291,6 +305,8 @@ hetcclResult_t hetccl_comm_export(hetcclComm_t c, void* blob, size_t* blob_bytes
   memcpy(b.map, c->map, sizeof(int) * c->n);
   b.slot_bytes = c->slot_bytes;
   b.nch_max = c->nch_max;
+  b.ws = c->ws;
+  b.nslots = c->nslots;
   DevGuard g(c->device);
   CUDA_TRY(c, cudaIpcGetMemHandle(&b.handle, c->local[0]));
   memset(blob, 0, HETCCL_BLOB_BYTES);
@@ -313,8 +329,8 @@ hetcclResult_t hetccl_comm_connect(hetcclComm_t c, const void* blobs, size_t blo
       return fail(c, hetcclInvalidUsage, "blob %d is not a hetccl blob for rank %d of %d", r, r, c->n);
     if (memcmp(b.map, c->map, sizeof(int) * c->n) != 0)
       return fail(c, hetcclInvalidUsage, "rank %d passed a different rank_to_domain map", r);
-    if (b.slot_bytes != c->slot_bytes || b.nch_max != c->nch_max)
-      return fail(c, hetcclInvalidUsage, "rank %d has different HETCCL_SLOT_KB/HETCCL_NCHANNELS", r);
+    if (b.slot_bytes != c->slot_bytes || b.nch_max != c->nch_max || b.ws != c->ws || b.nslots != c->nslots)
+      return fail(c, hetcclInvalidUsage, "rank %d has different HETCCL_SLOT_KB/NCHANNELS/WS/NSLOTS", r);
     if (r == c->rank) continue;
     void* p = nullptr;
     cudaError_t e = cudaIpcOpenMemHandle(&p, b.handle, cudaIpcMemLazyEnablePeerAccess);
@@ -391,7 +407,7 @@ hetcclResult_t hetccl_comm_init_mux(hetcclComm_t* comm, int nranks, const int* r
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cuda_device);
     c->nch_max = std::max(1, std::min(c->nch_max, sms / nranks));
-    c->alloc_bytes = kFlagsReserve + (size_t)c->nch_max * kNumSlots * c->slot_bytes;
+    c->alloc_bytes = kFlagsReserve + (size_t)c->nch_max * c->nslots * c->slot_bytes;
   }
   cudaError_t e = cudaSuccess;
   for (int r = 0; r < nranks && e == cudaSuccess; r++) e = alloc_region(c->alloc_bytes, &c->local[r]);
@@ -526,7 +542,7 @@ hetcclResult_t hetccl_plan_info(int nranks, const int* rank_to_domain, int rank,
   info->tile_elems = g.tile;
   info->ntiles = g.ntiles;
   info->nchannels = g.nch;
-  info->nslots = kNumSlots;
+  info->nslots = tmp.nslots;
   return hetcclSuccess;
 }
 

@@ -1,0 +1,252 @@
+"""Measurement report for SURVEY §8(d) (one JSON line per row), run under torchrun (one rank per GPU).
+
+  torchrun --nproc-per-node N tools/report.py --what ar_sweep|collectives|c4|c5|splits [--out FILE]
+
+* ar_sweep    : bf16 AR 1 MiB .. 1 GiB (C2), hetccl vs flat NCCL on the same buffers, at the split of N
+* splits      : bf16 AR 256 MiB at every split of N GPUs (1+1; 2+2, 1+3, 1+1+2, 4, singletons)
+* collectives : bf16 RS / AG / Broadcast at 256 MiB (C3 analogue), hetccl vs NCCL
+* c4          : 1.3e9-element gradients in 25 MiB buckets, issued round-robin on 1/2/4 streams (one comm per
+                stream), wall time per step vs NCCL
+* c5          : Llama-7B gradients (6,738,415,616 elements, 13.5 GB bf16 per rank) in 256 MiB buckets
+Times: CUDA events on the launching stream, max over ranks (R16). busBW per R15. Parity: each
+measured buffer is checked bitwise against the oracle on sampled windows (tests/ owns full parity).
+"""
+import argparse
+import json
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+SPLITS = {2: {"1+1": [0, 1], "2": [0, 0]},
+          4: {"2+2": [0, 0, 1, 1], "1+3": [0, 1, 1, 1], "1+1+2": [0, 1, 2, 2], "4": [0, 0, 0, 0],
+              "1+1+1+1": [0, 1, 2, 3]},
+          8: {"4+4": [0] * 4 + [1] * 4, "2+6": [0, 0] + [1] * 6, "2+2+4": [0, 0, 1, 1, 2, 2, 2, 2]}}
+DEFAULT = {2: "1+1", 4: "2+2", 8: "4+4"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--what", default="ar_sweep")
+    ap.add_argument("--out", default=None)
+    ap.add_argument("--iters", type=int, default=10)
+    args = ap.parse_args()
+    import torch
+    import torch.distributed as dist
+    import paper_2601_22585_b200 as hc
+    import oracle
+    import synth
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    gloo = dist.new_group(backend="gloo")
+    out = open(args.out, "a") if (args.out and rank == 0) else None
+    comms = {}
+
+    def comm_for(name, m, slot=0, nch=None):
+        key = (name, slot, nch)
+        if key not in comms:
+            old = os.environ.get("HETCCL_NCHANNELS")
+            if nch:
+                os.environ["HETCCL_NCHANNELS"] = str(nch)
+            comms[key] = hc.init_process_group_comm(m, group=gloo)
+            if nch:
+                if old is None:
+                    del os.environ["HETCCL_NCHANNELS"]
+                else:
+                    os.environ["HETCCL_NCHANNELS"] = old
+        return comms[key]
+
+    def emit(row):
+        if rank == 0:
+            line = json.dumps(row)
+            print(line, flush=True)
+            if out:
+                out.write(line + "\n")
+                out.flush()
+
+    def timed(fn, iters, warm=3, stream=None):
+        s = stream or torch.cuda.current_stream()
+        for _ in range(warm):
+            fn()
+        torch.cuda.synchronize()
+        dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        for _ in range(iters):
+            fn()
+        b.record(s)
+        torch.cuda.synchronize()
+        t = torch.tensor([a.elapsed_time(b) / iters], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.item() * 1e-3
+
+    def bf16_inputs(seed, count):
+        x = synth.normal(seed, rank, count, "bf16")
+        return torch.from_numpy(x.view(np.int16)).view(torch.bfloat16).to("cuda")
+
+    def parity_ar(y, seed, count, m):
+        W = 2048
+        ok = True
+        for st in (0, max(0, count // 2 - W // 2), max(0, count - W)):
+            w = min(W, count - st)
+            xs = [synth.normal(seed, r, w, "bf16", start=st) for r in range(world)]
+            want = oracle.allreduce(xs, m, "bf16", "sum")
+            got = y[st:st + w].cpu().view(torch.int16).numpy().view(np.uint16)
+            ok &= bool(np.array_equal(got, want))
+        t = torch.tensor([1 if ok else 0], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MIN)
+        return bool(t.item())
+
+    def ar_row(name, m, mib, seed=2, iters=None):
+        count = mib * (1 << 20) // 2
+        S = count * 2
+        x = bf16_inputs(seed, count)
+        y = torch.empty_like(x)
+        c = comm_for(name, m)
+        it = iters or (args.iters if mib <= 256 else max(3, args.iters // 4))
+        t = timed(lambda: hc.allreduce(x, y, c), it)
+        ok = parity_ar(y, seed, count, m)
+        z = x.clone()
+        tn = timed(lambda: dist.all_reduce(z), it)
+        alg = S / t / 1e9
+        bus = alg * 2 * (world - 1) / world
+        nbus = S / tn / 1e9 * 2 * (world - 1) / world
+        busiest = max(hc.hetccl_plan_info(m, r, hc.OP_ALLREDUCE, count, hc.BFLOAT16)["bytes_sent"] for r in range(world))
+        emit({"row": "allreduce", "split": name, "map": m, "n": world, "bytes": S, "dtype": "bf16", "ms": round(t * 1e3, 4),
+              "algbw": round(alg, 2), "busbw": round(bus, 2), "nccl_busbw": round(nbus, 2),
+              "vs_nccl": round(bus / nbus, 4), "busbw_over_900": round(bus / 900, 4),
+              "link_util_770": round(busiest / t / 1e9 / 770, 4), "parity_bitwise": ok})
+        del x, y, z
+
+    if args.what == "ar_sweep":
+        name = DEFAULT[world]
+        m = SPLITS[world][name]
+        for mib in [1, 2, 4, 8, 16, 32, 64, 128, 256, 512, 1024]:
+            ar_row(name, m, mib)
+    elif args.what == "splits":
+        for name, m in SPLITS[world].items():
+            ar_row(name, m, 256)
+    elif args.what == "collectives":
+        for name, m in SPLITS[world].items():
+            if world == 4 and name not in ("2+2", "1+3", "1+1+2"):
+                continue
+            c = comm_for(name, m)
+            S = 256 << 20
+            count = S // 2
+            R = count // world
+            x = bf16_inputs(3, count)
+            # reduce-scatter
+            y = torch.empty(R, dtype=torch.bfloat16, device="cuda")
+            t = timed(lambda: hc.reduce_scatter(x, y, c), args.iters)
+            W = 2048
+            xs = [synth.normal(3, r, count, "bf16") for r in range(world)] if rank == 0 else None
+            ok = True
+            if rank == 0:
+                want = oracle.reduce_scatter([v[:] for v in xs], m, "bf16", "sum")[0]
+                got = y.cpu().view(torch.int16).numpy().view(np.uint16)
+                ok = bool(np.array_equal(got[:W], want[:W]) and np.array_equal(got[-W:], want[-W:]))
+            yn = torch.empty_like(y)
+            tn = timed(lambda: dist.reduce_scatter_tensor(yn, x), args.iters)
+            f = (world - 1) / world
+            emit({"row": "reduce_scatter", "split": name, "n": world, "bytes": S, "ms": round(t * 1e3, 4),
+                  "busbw": round(S / t / 1e9 * f, 2), "nccl_busbw": round(S / tn / 1e9 * f, 2),
+                  "vs_nccl": round(tn / t, 4), "parity_bitwise_rank0": ok})
+            # all-gather
+            xa = x[:R].contiguous()
+            ya = torch.empty(count, dtype=torch.bfloat16, device="cuda")
+            t = timed(lambda: hc.all_gather(xa, ya, c), args.iters)
+            yn = torch.empty_like(ya)
+            tn = timed(lambda: dist.all_gather_into_tensor(yn, xa), args.iters)
+            ok = bool(torch.equal(ya.view(torch.int16), yn.view(torch.int16)))
+            emit({"row": "all_gather", "split": name, "n": world, "bytes": S, "ms": round(t * 1e3, 4),
+                  "busbw": round(S / t / 1e9 * f, 2), "nccl_busbw": round(S / tn / 1e9 * f, 2),
+                  "vs_nccl": round(tn / t, 4), "equals_nccl_bitwise": ok})
+            # broadcast (root = last rank)
+            yb = torch.empty_like(x)
+            root = world - 1
+            t = timed(lambda: hc.broadcast(x, yb, root, c), args.iters)
+            zb = x.clone()
+            tn = timed(lambda: dist.broadcast(zb, src=root), args.iters)
+            ok = bool(torch.equal(yb.view(torch.int16), zb.view(torch.int16)))
+            emit({"row": "broadcast", "split": name, "n": world, "bytes": S, "ms": round(t * 1e3, 4),
+                  "busbw": round(S / t / 1e9, 2), "nccl_busbw": round(S / tn / 1e9, 2), "vs_nccl": round(tn / t, 4),
+                  "equals_nccl_bitwise": ok})
+            del x, y, ya, yb, yn, zb
+    elif args.what == "c4":
+        name = {2: "1+1", 4: "1+1+2", 8: "2+2+4"}[world]
+        m = SPLITS[world][name]
+        total = 1_300_000_000
+        bucket = 25 * (1 << 20) // 2
+        sizes = [bucket] * (total // bucket) + ([total % bucket] if total % bucket else [])
+        g = bf16_inputs(4, total)
+        out_g = torch.empty_like(g)
+        offs = np.cumsum([0] + sizes)
+        for nstreams in (1, 2, 4):
+            streams = [torch.cuda.Stream() for _ in range(nstreams)]
+            # concurrent persistent kernels must be co-resident: split the SMs between the streams' comms
+            cs = [comm_for(name, m, slot=i, nch=148 // nstreams) for i in range(nstreams)]
+            cur = torch.cuda.current_stream()
+
+            def step():
+                for s in streams:
+                    s.wait_stream(cur)
+                for b, sz in enumerate(sizes):
+                    i = b % nstreams
+                    hc.hetccl_allreduce(g[offs[b]:].data_ptr(), out_g[offs[b]:].data_ptr(), int(sz), hc.BFLOAT16, "sum",
+                                        cs[i], streams[i].cuda_stream)
+                for s in streams:
+                    cur.wait_stream(s)
+            t = timed(step, 3, warm=1)
+            emit({"row": "c4_buckets", "split": name, "n": world, "streams": nstreams, "buckets": len(sizes),
+                  "bytes": total * 2, "ms": round(t * 1e3, 3),
+                  "eff_busbw": round(total * 2 / t / 1e9 * 2 * (world - 1) / world, 2)})
+        ok = parity_ar(out_g, 4, total, m)
+        z = g.clone()
+
+        def nstep():
+            for b, sz in enumerate(sizes):
+                dist.all_reduce(z[offs[b]:offs[b] + sz])
+        tn = timed(nstep, 3, warm=1)
+        emit({"row": "c4_buckets_nccl", "split": "flat", "n": world, "buckets": len(sizes), "bytes": total * 2,
+              "ms": round(tn * 1e3, 3), "eff_busbw": round(total * 2 / tn / 1e9 * 2 * (world - 1) / world, 2),
+              "hetccl_parity_bitwise": ok})
+    elif args.what == "c5":
+        name = DEFAULT[world]
+        m = SPLITS[world][name]
+        total = 6_738_415_616
+        bucket = 256 * (1 << 20) // 2
+        sizes = [bucket] * (total // bucket) + ([total % bucket] if total % bucket else [])
+        g = torch.empty(total, dtype=torch.bfloat16, device="cuda")
+        g.normal_(0, 1.0 / 16, generator=torch.Generator("cuda").manual_seed(5 + rank))
+        c = comm_for(name, m)
+        offs = np.cumsum([0] + sizes)
+
+        def step():
+            for b, sz in enumerate(sizes):
+                p = g[offs[b]:].data_ptr()
+                hc.hetccl_allreduce(p, p, int(sz), hc.BFLOAT16, "sum", c, torch.cuda.current_stream().cuda_stream)
+        t = timed(step, 2, warm=1)
+
+        def nstep():
+            for b, sz in enumerate(sizes):
+                dist.all_reduce(g[offs[b]:offs[b] + sz])
+        tn = timed(nstep, 2, warm=1)
+        S = total * 2
+        emit({"row": "c5_llama7b", "split": name, "n": world, "buckets": len(sizes), "bytes": S, "ms": round(t * 1e3, 2),
+              "eff_busbw": round(S / t / 1e9 * 2 * (world - 1) / world, 2), "nccl_ms": round(tn * 1e3, 2),
+              "nccl_eff_busbw": round(S / tn / 1e9 * 2 * (world - 1) / world, 2), "vs_nccl": round(tn / t, 4),
+              "note": "in-place; values grow across repeated steps (timing only; parity in tests)"})
+    for c in comms.values():
+        hc.hetccl_comm_destroy(c)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
