@@ -291,6 +291,112 @@ __device__ __noinline__ void cta_fold(const PtrList& srcs, const PtrList& dsts, 
   }
 }
 
+// Two-level fold (the hierarchy of reading R3/R6 in one pass):
+//   P_kpos = narrow( fold_{s in order} widen(inner[s][i]) ), P_q = outer[q][i] for q != kpos,
+//   dst[d][i] = narrow( fold_{q < outer.n in order} widen(P_q) ) for every destination d.
+// Used where a rank owns both its domain's partial and the cross-domain result of an element, so the
+// partial never round-trips through memory. Bitwise identical to cta_fold of inner, stored, then
+// cta_fold of outer.
+template <typename T, int OP>
+__device__ __noinline__ void cta_fold_hier(const PtrList& inner, int kpos, const PtrList& outer, const PtrList& dsts,
+                                           size_t n) {
+  using TR = Tr<T>;
+  using S = typename TR::S;
+  using A = typename TR::A;
+  constexpr int V = TR::V;
+  if (n == 0) return;
+  const int tid = (int)threadIdx.x - g_dbase, nth = g_dnth;
+  const int D = outer.n;
+  uintptr_t al = 0;
+  for (int q = 0; q < D; q++)
+    if (q != kpos) al |= (uintptr_t)outer.p[q];
+  const size_t nv = (all_aligned16(inner, dsts) && (al & 15) == 0) ? n / V : 0;
+  for (size_t v0 = tid; v0 < nv; v0 += (size_t)kUnroll * nth) {
+    A acc[kUnroll][V];
+    uint4 pk[kUnroll];
+    // ---- inner fold -> P_kpos (narrowed, kept packed) ----
+    for (int s = 0; s < inner.n; s++) {
+      uint4 w[kUnroll];
+      const char* sp = (const char*)inner.p[s];
+#pragma unroll
+      for (int u = 0; u < kUnroll; u++) {
+        size_t v = v0 + (size_t)u * nth;
+        if (v < nv) w[u] = ld_v4(sp + v * 16);
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; u++)
+#pragma unroll
+        for (int e = 0; e < V; e++) {
+          const A x = TR::widen(Vec<S>::get(w[u], e));
+          acc[u][e] = s == 0 ? x : comb<OP>(acc[u][e], x);
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; u++)
+#pragma unroll
+      for (int e = 0; e < V; e++) Vec<S>::set(pk[u], e, TR::narrow(acc[u][e]));
+    // ---- outer fold over the D domain partials in ascending order ----
+    for (int q = 0; q < D; q++) {
+      if (q == kpos) {
+#pragma unroll
+        for (int u = 0; u < kUnroll; u++)
+#pragma unroll
+          for (int e = 0; e < V; e++) {
+            const A x = TR::widen(Vec<S>::get(pk[u], e));
+            acc[u][e] = q == 0 ? x : comb<OP>(acc[u][e], x);
+          }
+        continue;
+      }
+      uint4 w[kUnroll];
+      const char* sp = (const char*)outer.p[q];
+#pragma unroll
+      for (int u = 0; u < kUnroll; u++) {
+        size_t v = v0 + (size_t)u * nth;
+        if (v < nv) w[u] = ld_v4(sp + v * 16);
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; u++)
+#pragma unroll
+        for (int e = 0; e < V; e++) {
+          const A x = TR::widen(Vec<S>::get(w[u], e));
+          acc[u][e] = q == 0 ? x : comb<OP>(acc[u][e], x);
+        }
+    }
+    uint4 o[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; u++)
+#pragma unroll
+      for (int e = 0; e < V; e++) Vec<S>::set(o[u], e, TR::narrow(acc[u][e]));
+    for (int d = 0; d < dsts.n; d++) {
+      char* dp = (char*)dsts.p[d];
+#pragma unroll
+      for (int u = 0; u < kUnroll; u++) {
+        size_t v = v0 + (size_t)u * nth;
+        if (v < nv) st_v4(dp + v * 16, o[u]);
+      }
+    }
+  }
+  for (size_t i = nv * V + tid; i < n; i += nth) {
+    A a = 0;
+    for (int s = 0; s < inner.n; s++) {
+      S w = sizeof(S) == 4 ? (S)ld_s32((const char*)inner.p[s] + i * 4) : (S)ld_s16((const char*)inner.p[s] + i * 2);
+      a = s == 0 ? TR::widen(w) : comb<OP>(a, TR::widen(w));
+    }
+    const S pks = TR::narrow(a);
+    for (int q = 0; q < D; q++) {
+      S w = q == kpos ? pks
+                      : (sizeof(S) == 4 ? (S)ld_s32((const char*)outer.p[q] + i * 4)
+                                        : (S)ld_s16((const char*)outer.p[q] + i * 2));
+      a = q == 0 ? TR::widen(w) : comb<OP>(a, TR::widen(w));
+    }
+    S r = TR::narrow(a);
+    for (int d = 0; d < dsts.n; d++) {
+      if (sizeof(S) == 4) st_s32((char*)dsts.p[d] + i * 4, (uint32_t)r);
+      else st_s16((char*)dsts.p[d] + i * 2, (uint16_t)r);
+    }
+  }
+}
+
 // ------------------------------------------------------------------ protocol helpers -----------
 __device__ __forceinline__ uint64_t* chan_flags(const OpArgs& a, int rank, int ch) {
   return a.mem[rank].flags + (size_t)ch * kChanWords;
@@ -532,8 +638,9 @@ __device__ __forceinline__ void run_pipeline(const OpArgs& a, Op& op, int me, in
 // Slot layout on a rank of domain k (d = d_k, Rk = tile/d; s1/s3 have one entry per domain PEER,
 // compact index cidx(i, j)):
 //   s1[d-1][Rk] | s2[D][Rk] | ag[Rk] | s3[d-1][Rk]
-// Stages: 0 A intra push | 1 B intra fold + cross push | 2 C cross fold + AG push |
-//         3 D final region -> y and domain peers | 4 E domain peers' regions -> y
+// Stages: 0 A intra push | 1 B domain fold of the other domains' pieces + cross push |
+//         2 C domain fold of my pieces + cross fold -> y, other owners' ag, domain peers' s3 |
+//         3 D other owners' pieces (ag) -> y and domain peers | 4 E domain peers' regions -> y
 template <typename T, int OP>
 struct ArOp {
   static constexpr int ES = sizeof(T);
@@ -581,9 +688,10 @@ struct ArOp {
         const size_t p0 = g.seg(i * spj), p1 = g.seg((i + 1) * spj);
         cta_copy1<ES>(x + tb + p0, slot_ptr<T>(a, peer(i), ch, slot) + (size_t)cidx(j, i) * Rk, p1 - p0);
       }
-    } else if (s == 1) {  // ---- B: fold my region over the domain; route each piece to its reducer ----
+    } else if (s == 1) {  // ---- B: fold the other domains' pieces of my region; push to their reducers ----
       for (int sg = s_lo; sg < s_hi; sg++) {
         for (int q = 0; q < D; q++) {
+          if (D > 1 && q == k) continue;  // my own piece is folded in C (its partial never leaves registers)
           const size_t c0 = g.piece(sg, q), c1 = g.piece(sg, q + 1);
           if (c1 <= c0) continue;
           PtrList src, dst;
@@ -591,8 +699,6 @@ struct ArOp {
             src.add(i == j ? (const void*)(x + tb + c0) : (const void*)(mine + (size_t)cidx(i, j) * Rk + (c0 - r0)));
           if (D == 1) {
             dst.add(y + tb + c0);
-          } else if (q == k) {
-            dst.add(my_s2 + (size_t)k * Rk + (c0 - r0));
           } else {
             const int o = owner_of(tp, q, sg);
             const int dq = tp.dom_size[q];
@@ -601,12 +707,14 @@ struct ArOp {
           cta_fold<T, OP>(src, dst, c1 - c0);
         }
       }
-    } else if (s == 2) {  // ---- C: fold the D partials of my pieces; final piece -> y and other owners ----
+    } else if (s == 2) {  // ---- C: P_k of my pieces (domain fold) + the other partials; final -> y, owners, peers ----
       for (int sg = s_lo; sg < s_hi; sg++) {
         const size_t c0 = g.piece(sg, k), c1 = g.piece(sg, k + 1);
         if (c1 <= c0) continue;
-        PtrList src, dst;
-        for (int q = 0; q < D; q++) src.add(my_s2 + (size_t)q * Rk + (c0 - r0));
+        PtrList inner, outer, dst;
+        for (int i = 0; i < d; i++)
+          inner.add(i == j ? (const void*)(x + tb + c0) : (const void*)(mine + (size_t)cidx(i, j) * Rk + (c0 - r0)));
+        for (int q = 0; q < D; q++) outer.add(q == k ? nullptr : (const void*)(my_s2 + (size_t)q * Rk + (c0 - r0)));
         dst.add(y + tb + c0);
         for (int q = 0; q < D; q++) {
           if (q == k) continue;
@@ -614,9 +722,13 @@ struct ArOp {
           const int dq = tp.dom_size[q];
           dst.add(slot_ptr<T>(a, o, ch, slot) + s2_off(dq) + (size_t)D * (TL / dq) + (c0 - region_lo(g, o)));
         }
-        cta_fold<T, OP>(src, dst, c1 - c0);
+        for (int i = 0; i < d; i++)
+          if (i != j)
+            dst.add(slot_ptr<T>(a, peer(i), ch, slot) + s2_off(d) + (size_t)(D + 1) * Rk + (size_t)cidx(j, i) * Rk +
+                    (c0 - r0));
+        cta_fold_hier<T, OP>(inner, k, outer, dst, c1 - c0);
       }
-    } else if (s == 3) {  // ---- D: my final region -> y (pieces from other owners) and to domain peers ----
+    } else if (s == 3) {  // ---- D: the other owners' final pieces of my region -> y and domain peers ----
       PtrList peers_s3;
       for (int i = 0; i < d; i++)
         if (i != j) peers_s3.add(slot_ptr<T>(a, peer(i), ch, slot) + s2_off(d) + (size_t)(D + 1) * Rk + (size_t)cidx(j, i) * Rk);
@@ -625,16 +737,13 @@ struct ArOp {
       } else {
         for (int sg = s_lo; sg < s_hi; sg++) {
           for (int q = 0; q < D; q++) {
+            if (q == k) continue;  // pushed to the peers by C
             const size_t c0 = g.piece(sg, q), c1 = g.piece(sg, q + 1);
             if (c1 <= c0) continue;
             PtrList dst;
+            dst.add(y + tb + c0);
             for (int i = 0; i < peers_s3.n; i++) dst.add((const char*)peers_s3.p[i] + (c0 - r0) * ES);
-            if (q == k) {
-              if (dst.n) cta_copy<ES>(y + tb + c0, dst, c1 - c0);
-            } else {
-              dst.add(y + tb + c0);
-              cta_copy<ES>(my_ag + (c0 - r0), dst, c1 - c0);
-            }
+            cta_copy<ES>(my_ag + (c0 - r0), dst, c1 - c0);
           }
         }
       }
@@ -652,7 +761,8 @@ struct ArOp {
 // Per tile (per-shard offsets [tb, tb+len)), member j of domain k owns: its own shard, plus piece j
 // (of d) of every other-domain shard. Slot layout on a rank of domain k (RG = T + (n-d)*T/d):
 //   s1[d-1][RG] | s2[D][T]  (s1[cidx(i,j)]: own-shard part at 0, other-domain shard #ro at T + ro*T/d)
-// Stages: 0 A intra push | 1 B domain fold + cross push | 2 C cross fold -> y
+// Stages: 0 A intra push | 1 B domain fold of other shards' pieces + cross push |
+//         2 C domain fold of my shard + cross fold -> y
 template <typename T, int OP>
 struct RsOp {
   static constexpr int ES = sizeof(T);
@@ -696,12 +806,11 @@ struct RsOp {
         }
       }
     } else if (s == 1) {  // ---- B: own shard -> domain partial; my pieces of other shards -> their owners ----
-      {
+      if (D == 1) {  // one domain: the domain fold is the result (with D > 1 it is folded in C)
         PtrList src, dst;
         for (int i = 0; i < d; i++)
           src.add(i == j ? (const void*)(x + (size_t)me * R + tb) : (const void*)(mine + (size_t)cidx(i, j) * RG));
-        if (D == 1) dst.add(y + tb);
-        else dst.add(mine + (size_t)(d - 1) * RG + (size_t)k * TL);
+        dst.add(y + tb);
         cta_fold<T, OP>(src, dst, len);
       }
       int ro = 0;
@@ -717,11 +826,14 @@ struct RsOp {
         cta_fold<T, OP>(src, dst, pj1 - pj0);
         ro++;
       }
-    } else {  // ---- C: fold the D domain partials of my shard (ascending domain id) ----
-      PtrList src, dst;
-      for (int q = 0; q < D; q++) src.add(mine + (size_t)(d - 1) * RG + (size_t)q * TL);
+    } else {  // ---- C: my domain's partial of my shard + the D-1 others (ascending domain id) -> y ----
+      PtrList inner, outer, dst;
+      for (int i = 0; i < d; i++)
+        inner.add(i == j ? (const void*)(x + (size_t)me * R + tb) : (const void*)(mine + (size_t)cidx(i, j) * RG));
+      for (int q = 0; q < D; q++)
+        outer.add(q == k ? nullptr : (const void*)(mine + (size_t)(d - 1) * RG + (size_t)q * TL));
       dst.add(y + tb);
-      cta_fold<T, OP>(src, dst, len);
+      cta_fold_hier<T, OP>(inner, k, outer, dst, len);
     }
   }
 };
