@@ -12,7 +12,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_HERE, "libhetccl.so")
+# HETCCL_LIB selects an in-tree build variant (A/B experiments); default libhetccl.so
+_LIB_PATH = os.path.join(_HERE, os.environ.get("HETCCL_LIB", "libhetccl.so"))
 
 INT32, FLOAT16, FLOAT32, BFLOAT16 = 2, 6, 7, 9
 SUM, MAX, MIN = 0, 2, 3

@@ -26,21 +26,23 @@ def stale():
     return any(os.path.getmtime(f) > t for f in files)
 
 
-def build(force=False, verbose=False):
-    if not force and not stale():
+def build(force=False, verbose=False, variant=None, defines=()):
+    """Build libhetccl.so (or, for A/B experiments, libhetccl_<variant>.so with extra -D defines)."""
+    lib = LIB if not variant else os.path.join(HERE, f"libhetccl_{variant}.so")
+    if not force and not variant and not stale():
         return LIB
-    tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *FLAGS, "-o", tmp] + [os.path.join(CSRC, s) for s in SOURCES]
+    tmp = lib + f".tmp{os.getpid()}"
+    cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-o", tmp] + [os.path.join(CSRC, s) for s in SOURCES]
     p = subprocess.run(cmd, capture_output=True, text=True)
     if p.returncode != 0:
         sys.stderr.write(p.stdout + p.stderr)
         raise RuntimeError("nvcc failed building libhetccl.so")
-    with open(os.path.join(HERE, "ptxas_info.txt"), "w") as f:
+    with open(os.path.join(HERE, "ptxas_info.txt" if not variant else f"ptxas_info_{variant}.txt"), "w") as f:
         f.write(p.stderr)
     if verbose:
         sys.stderr.write(p.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":

@@ -21,7 +21,10 @@ namespace hetccl {
 constexpr int kMaxRanks = 16;      // == HETCCL_MAX_RANKS (one flag line = 16 senders x 8 B)
 constexpr int kMaxChannels = 148;  // hard cap on CTAs per rank per op (one per SM)
 constexpr int kMaxSlots = 16;      // cap on the scratch ring depth per channel (HETCCL_NSLOTS)
-constexpr int kThreads = 512;      // threads per CTA
+#ifndef HETCCL_THREADS
+#define HETCCL_THREADS 512
+#endif
+constexpr int kThreads = HETCCL_THREADS;  // threads per CTA (one CTA per SM)
 constexpr int kMaxStages = 5;      // pipeline positions of the deepest op (All-Reduce)
 
 // counters (per rank, per channel); C_ACK counts tiles a sender has fully consumed
