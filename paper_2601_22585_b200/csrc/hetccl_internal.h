@@ -22,7 +22,7 @@ constexpr int kMaxRanks = 16;      // == HETCCL_MAX_RANKS (one flag line = 16 se
 constexpr int kMaxChannels = 148;  // hard cap on CTAs per rank per op (one per SM)
 constexpr int kMaxSlots = 16;      // cap on the scratch ring depth per channel (HETCCL_NSLOTS)
 #ifndef HETCCL_THREADS
-#define HETCCL_THREADS 512
+#define HETCCL_THREADS 256
 #endif
 constexpr int kThreads = HETCCL_THREADS;  // threads per CTA (one CTA per SM)
 constexpr int kMaxStages = 5;      // pipeline positions of the deepest op (All-Reduce)

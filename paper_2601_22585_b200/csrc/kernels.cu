@@ -172,8 +172,14 @@ __device__ __forceinline__ bool all_aligned16(const PtrList& a, const PtrList& b
 // to the flag protocol), read by the data movers
 __shared__ int g_dbase, g_dnth;
 
-constexpr int kUnroll = 4;      // vectors in flight per thread per source in a fold
-constexpr int kCopyUnroll = 8;  // vectors in flight per thread in a copy
+#ifndef HETCCL_FOLD_UNROLL
+#define HETCCL_FOLD_UNROLL 4
+#endif
+#ifndef HETCCL_COPY_UNROLL
+#define HETCCL_COPY_UNROLL 8
+#endif
+constexpr int kUnroll = HETCCL_FOLD_UNROLL;      // vectors in flight per thread per source in a fold
+constexpr int kCopyUnroll = HETCCL_COPY_UNROLL;  // vectors in flight per thread in a copy
 
 // dst[d][i] = src[i] for every destination d, i < n elements of size ES (bit copy)
 template <int ES>
