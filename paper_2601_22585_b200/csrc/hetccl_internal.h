@@ -8,7 +8,7 @@
 //             (red.release... see kernels.cu), polled locally (ld.acquire.sys), one lane per sender.
 //   base    : same shape; this rank's own cumulative "expected so far" per (channel, counter,
 //             sender), advanced by each launch at exit, plus the channel's cumulative tile count in
-//             word 0 of counter line kCounters. Targets are cumulative across launches, so the
+//             word 0 and its cumulative one-shot op count in word 1 of counter line kCounters. Targets are cumulative across launches, so the
 //             protocol needs no host sequence numbers and survives CUDA-graph replay.
 //   scratch : [channel][slot] ring of nslots (<= kMaxSlots) slots of slot_elems elements; slot g % nslots
 //             holds every staging buffer cumulative tile g of that channel needs on this rank.
@@ -28,13 +28,21 @@ constexpr int kThreads = HETCCL_THREADS;  // threads per CTA (one CTA per SM)
 constexpr int kMaxStages = 5;      // pipeline positions of the deepest op (All-Reduce)
 
 // counters (per rank, per channel); C_ACK counts tiles a sender has fully consumed
-enum : int { C_S1 = 0, C_S2 = 1, C_AG = 2, C_S3 = 3, C_ACK = 4, kCounters = 5, C_NONE = 7 };
+// C_OS / C_OSACK belong to the one-shot small-message All-Reduce (k_allreduce_oneshot).
+enum : int { C_S1 = 0, C_S2 = 1, C_AG = 2, C_S3 = 3, C_ACK = 4, C_OS = 5, C_OSACK = 6, kCounters = 7, C_NONE = 7 };
 constexpr size_t kLineWords = 16;  // uint64 words per 128-B line
 constexpr size_t kChanWords = (size_t)(kCounters + 1) * kLineWords;  // + one line of channel state
 constexpr size_t kFlagsBytes = (size_t)kMaxChannels * kChanWords * sizeof(uint64_t);
 constexpr size_t kFlagsReserve = 2 * ((kFlagsBytes + 65535) / 65536) * 65536;  // flags + base, 64K aligned
 
-enum OpKind : int { OP_ALLREDUCE = 0, OP_REDUCE_SCATTER = 1, OP_ALL_GATHER = 2, OP_BROADCAST = 3, OP_COPY = 4 };
+enum OpKind : int {
+  OP_ALLREDUCE = 0,
+  OP_REDUCE_SCATTER = 1,
+  OP_ALL_GATHER = 2,
+  OP_BROADCAST = 3,
+  OP_COPY = 4,
+  OP_ALLREDUCE_ONESHOT = 5  // small-message All-Reduce (NEXT-3), same result as OP_ALLREDUCE
+};
 enum DType : int { DT_INT32 = 2, DT_F16 = 6, DT_F32 = 7, DT_BF16 = 9 };
 enum RedOp : int { RED_SUM = 0, RED_MAX = 2, RED_MIN = 3 };
 
@@ -95,6 +103,8 @@ struct OpArgs {
   int trace_iters;
   int ws;                       // 0: plain pipeline; k >= 2: warp-specialised, consumers k positions after producers
   int nslots;                   // scratch ring depth (> pipeline positions)
+  size_t os_off;                // one-shot area: byte offset in every rank's scratch, bytes per (buffer, sender)
+  size_t os_stride;
 };
 
 // ---- host plan (plan.cpp) ----

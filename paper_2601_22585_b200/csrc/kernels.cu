@@ -403,6 +403,81 @@ __device__ __noinline__ void cta_fold_hier(const PtrList& inner, int kpos, const
   }
 }
 
+// Multi-level fold over ALL ranks in the oracle's order (readings R3, R5, R6): srcs[r] is rank r's
+// operand; P_q = fold over domain q's members (ascending rank), narrowed iff D > 1; result = fold of
+// the P_q in ascending domain id, narrowed. The one-shot All-Reduce's reduction.
+template <typename T, int OP>
+__device__ __forceinline__ void cta_fold_domains(const PtrList& srcs, const Topo& tp, const PtrList& dsts, size_t n) {
+  using TR = Tr<T>;
+  using S = typename TR::S;
+  using A = typename TR::A;
+  constexpr int V = TR::V;
+  if (n == 0) return;
+  const int tid = (int)threadIdx.x - g_dbase, nth = g_dnth;
+  const size_t nv = all_aligned16(srcs, dsts) ? n / V : 0;
+  const int D = tp.D;
+  for (size_t v0 = tid; v0 < nv; v0 += (size_t)kUnroll * nth) {
+    A out[kUnroll][V], acc[kUnroll][V];
+    for (int q = 0; q < D; q++) {
+      const int d = tp.dom_size[q];
+      for (int i = 0; i < d; i++) {
+        uint4 w[kUnroll];
+        const char* sp = (const char*)srcs.p[tp.members[tp.dom_first[q] + i]];
+#pragma unroll
+        for (int u = 0; u < kUnroll; u++) {
+          size_t v = v0 + (size_t)u * nth;
+          if (v < nv) w[u] = ld_v4(sp + v * 16);
+        }
+#pragma unroll
+        for (int u = 0; u < kUnroll; u++)
+#pragma unroll
+          for (int e = 0; e < V; e++) {
+            const A x = TR::widen(Vec<S>::get(w[u], e));
+            acc[u][e] = i == 0 ? x : comb<OP>(acc[u][e], x);
+          }
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; u++)
+#pragma unroll
+        for (int e = 0; e < V; e++) {
+          const A p = D > 1 ? TR::widen(TR::narrow(acc[u][e])) : acc[u][e];
+          out[u][e] = q == 0 ? p : comb<OP>(out[u][e], p);
+        }
+    }
+    uint4 o[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; u++)
+#pragma unroll
+      for (int e = 0; e < V; e++) Vec<S>::set(o[u], e, TR::narrow(out[u][e]));
+    for (int d = 0; d < dsts.n; d++) {
+      char* dp = (char*)dsts.p[d];
+#pragma unroll
+      for (int u = 0; u < kUnroll; u++) {
+        size_t v = v0 + (size_t)u * nth;
+        if (v < nv) st_v4(dp + v * 16, o[u]);
+      }
+    }
+  }
+  for (size_t i = nv * V + tid; i < n; i += nth) {
+    A out = 0;
+    for (int q = 0; q < D; q++) {
+      A acc = 0;
+      for (int k = 0; k < tp.dom_size[q]; k++) {
+        const char* sp = (const char*)srcs.p[tp.members[tp.dom_first[q] + k]];
+        S w = sizeof(S) == 4 ? (S)ld_s32(sp + i * 4) : (S)ld_s16(sp + i * 2);
+        acc = k == 0 ? TR::widen(w) : comb<OP>(acc, TR::widen(w));
+      }
+      const A p = D > 1 ? TR::widen(TR::narrow(acc)) : acc;
+      out = q == 0 ? p : comb<OP>(out, p);
+    }
+    S r = TR::narrow(out);
+    for (int d = 0; d < dsts.n; d++) {
+      if (sizeof(S) == 4) st_s32((char*)dsts.p[d] + i * 4, (uint32_t)r);
+      else st_s16((char*)dsts.p[d] + i * 2, (uint16_t)r);
+    }
+  }
+}
+
 // ------------------------------------------------------------------ protocol helpers -----------
 __device__ __forceinline__ uint64_t* chan_flags(const OpArgs& a, int rank, int ch) {
   return a.mem[rank].flags + (size_t)ch * kChanWords;
@@ -1030,6 +1105,87 @@ __global__ void __launch_bounds__(kThreads, 1) k_broadcast(const __grid_constant
   run_pipeline(a, op, op.me, blockIdx.x);
 }
 
+// ================================================================== one-shot All-Reduce (NEXT-3) =
+// Small messages are latency-bound: the five-stage hierarchy costs five flag round trips. Here every
+// rank pushes its whole chunk into every peer's one-shot area (double-buffered by op parity), signals
+// once, waits for the n-1 others, and reduces all n operands locally in the oracle's domain-major
+// order (cta_fold_domains) — bitwise identical to the hierarchical path, one round trip.
+// Counters per (channel, sender): C_OS (data of op g landed), C_OSACK (op g's buffer consumed).
+template <typename T, int OP>
+__global__ void __launch_bounds__(kThreads, 1) k_allreduce_oneshot(const __grid_constant__ OpArgs a) {
+  constexpr int V = Tr<T>::V;
+  const int row = blockIdx.y, ch = blockIdx.x;
+  const int me = a.local_rank[row], n = a.topo.n;
+  const T* x = (const T*)a.send[row];
+  T* y = (T*)a.recv[row];
+  uint64_t* F = chan_flags(a, me, ch);
+  uint64_t* B = chan_base(a, me, ch);
+  __shared__ unsigned long long ops0;
+  __shared__ int abort_;
+  if (threadIdx.x == 0) {
+    ops0 = B[kCounters * kLineWords + 1];
+    abort_ = 0;
+    g_dbase = 0;
+    g_dnth = blockDim.x;
+  }
+  __syncthreads();
+  const unsigned long long g = ops0;
+  const int buf = (int)(g & 1);
+  const size_t chunk = (a.count + (size_t)a.nch * V - 1) / ((size_t)a.nch * V) * V;
+  const size_t lo = min(a.count, (size_t)ch * chunk), hi = min(a.count, lo + chunk);
+  auto area = [&](int owner, int sender) -> T* {
+    return (T*)(a.mem[owner].scratch + a.os_off + ((size_t)buf * n + sender) * a.os_stride);
+  };
+  auto wait_all = [&](int ctr, uint64_t target) {
+    if (threadIdx.x < 32) {
+      const int lane = threadIdx.x;
+      if (lane < n && lane != me) {
+        const uint64_t* w = F + ctr * kLineWords + lane;
+        const uint64_t t0 = globaltimer();
+        uint32_t spins = 0;
+        while (ld_acquire_sys(w) < target) {
+          if ((++spins & 1023u) == 0 && (long long)(globaltimer() - t0) > a.timeout_ns) {
+            atomicOr(a.err, 1ull + ((unsigned long long)ctr << 8) + ((unsigned long long)lane << 16));
+            abort_ = 1;
+            break;
+          }
+        }
+      }
+    }
+    __syncthreads();
+  };
+  auto signal_all = [&](int ctr) {
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      fence_acq_rel_sys();
+      const int lane = threadIdx.x;
+      if (lane < n && lane != me) red_add_relaxed_sys(chan_flags(a, lane, ch) + ctr * kLineWords + me, 1);
+    }
+  };
+  // 1. the buffer of op g-2 must be consumed everywhere before it is overwritten
+  if (g >= 2) wait_all(C_OSACK, g - 1);
+  if (abort_) return;
+  // 2. push my chunk to every peer
+  {
+    PtrList dst;
+    for (int r = 0; r < n; r++)
+      if (r != me) dst.add(area(r, me) + lo);
+    cta_copy<sizeof(T)>(x + lo, dst, hi - lo);
+  }
+  signal_all(C_OS);
+  // 3. wait for every peer's chunk, reduce all n operands in the oracle's order
+  wait_all(C_OS, g + 1);
+  if (abort_) return;
+  {
+    PtrList src, dst;
+    for (int r = 0; r < n; r++) src.add(r == me ? (const void*)(x + lo) : (const void*)(area(me, r) + lo));
+    dst.add(y + lo);
+    cta_fold_domains<T, OP>(src, a.topo, dst, hi - lo);
+  }
+  signal_all(C_OSACK);  // my reads of this buffer are done
+  if (threadIdx.x == 0) B[kCounters * kLineWords + 1] = g + 1;
+}
+
 // ================================================================== n = 1 (a9) ================
 template <int ES>
 __global__ void __launch_bounds__(kThreads) k_copy(const void* src, void* dst, size_t n) {
@@ -1054,6 +1210,21 @@ __global__ void __launch_bounds__(kThreads) k_copy(const void* src, void* dst, s
 
 // ================================================================== launch ====================
 typedef void (*KernFn)(OpArgs);
+
+static KernFn pick_oneshot(int dt, int red) {
+#define HC_OS(T)                                                       \
+  if (red == RED_SUM) return (KernFn)k_allreduce_oneshot<T, RED_SUM>; \
+  if (red == RED_MAX) return (KernFn)k_allreduce_oneshot<T, RED_MAX>; \
+  return (KernFn)k_allreduce_oneshot<T, RED_MIN>;
+  switch (dt) {
+    case DT_F32: { HC_OS(float) }
+    case DT_INT32: { HC_OS(int32_t) }
+    case DT_BF16: { HC_OS(__nv_bfloat16) }
+    case DT_F16: { HC_OS(__half) }
+  }
+#undef HC_OS
+  return nullptr;
+}
 
 template <typename T>
 static KernFn pick_reduce(int op, int red) {
@@ -1084,7 +1255,7 @@ static KernFn pick(int op, int dt, int red) {
 }
 
 cudaError_t launch_collective(const OpArgs& a, int nlocal, int dt, int red, bool cooperative, cudaStream_t s) {
-  KernFn fn = pick(a.op, dt, red);
+  KernFn fn = a.op == OP_ALLREDUCE_ONESHOT ? pick_oneshot(dt, red) : pick(a.op, dt, red);
   if (!fn) return cudaErrorInvalidValue;
   dim3 grid(a.nch, nlocal), block(kThreads);
   void* args[] = {(void*)&a};
@@ -1104,7 +1275,7 @@ cudaError_t launch_copy(const void* src, void* dst, size_t n, int es, cudaStream
 
 // max co-resident CTAs of a collective kernel on this device (for the cooperative mux launch)
 int max_coresident(int op, int dt, int red) {
-  KernFn fn = pick(op, dt, red);
+  KernFn fn = op == OP_ALLREDUCE_ONESHOT ? pick_oneshot(dt, red) : pick(op, dt, red);
   int per_sm = 0, dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

@@ -41,6 +41,8 @@ struct hetcclComm {
   int trace_iters = 0;                    // HETCCL_TRACE_ITERS: per-iteration timestamps of the last op
   int ws = 0;                             // HETCCL_WS: 0 plain pipeline, k in 2..4 warp-specialised (spacing k)
   int nslots = 8;                         // HETCCL_NSLOTS: scratch ring depth
+  size_t os_bytes = 0;                    // HETCCL_ONESHOT_KB: one-shot AR up to this many bytes per rank
+  size_t os_stride = 0;                   // bytes per (buffer, sender) of the one-shot area
   unsigned long long* trace = nullptr;
   size_t trace_bytes = 0;
   int trace_shape[2] = {0, 0};            // local ranks, channels of the last traced op
@@ -58,7 +60,7 @@ struct Blob {
   int nch_max;
   int ws;
   int nslots;
-  int pad;
+  unsigned long long os_bytes;
   cudaIpcMemHandle_t handle;
 };
 static_assert(sizeof(Blob) <= HETCCL_BLOB_BYTES, "blob too large");
@@ -87,6 +89,12 @@ long env_long(const char* name, long dflt) {
   return e && *e ? atol(e) : dflt;
 }
 
+// [flags | base | nch_max x nslots slots | one-shot area: 2 buffers x n senders x os_stride]
+size_t scratch_slots_bytes(const hetcclComm* c) { return (size_t)c->nch_max * c->nslots * c->slot_bytes; }
+size_t alloc_bytes_for(const hetcclComm* c) {
+  return kFlagsReserve + scratch_slots_bytes(c) + 2 * (size_t)c->topo.n * c->os_stride;
+}
+
 void read_env(hetcclComm* c) {
   c->nch_max = (int)std::max(1L, std::min((long)kMaxChannels, env_long("HETCCL_NCHANNELS", 128)));
   // scratch slot: HETCCL_SLOT_KB, else sized from this map so every op's default tile fits
@@ -100,7 +108,9 @@ void read_env(hetcclComm* c) {
   if (c->ws == 1 || c->ws < 0) c->ws = 0;
   if (c->ws > 4) c->ws = 4;
   c->nslots = (int)std::max(2L, std::min((long)kMaxSlots, env_long("HETCCL_NSLOTS", 8)));
-  c->alloc_bytes = kFlagsReserve + (size_t)c->nch_max * c->nslots * c->slot_bytes;
+  c->os_bytes = (size_t)std::max(0L, env_long("HETCCL_ONESHOT_KB", 1024)) * 1024;
+  c->os_stride = (c->os_bytes + 255) / 256 * 256;
+  c->alloc_bytes = alloc_bytes_for(c);
 }
 
 // allocate one rank's [flags | scratch] region on the current device, flags zeroed
@@ -177,6 +187,7 @@ hetcclResult_t run_op(hetcclComm_t c, int op, const void* const* sends, void* co
     CUDA_TRY(c, launch_copy(sends[0], recvs[0], recv_elems(op, count, 1), es, stream));
     return hetcclSuccess;
   }
+  const bool oneshot = op == OP_ALLREDUCE && c->os_bytes > 0 && count * (size_t)es <= c->os_bytes;
   OpArgs a;
   memset(&a, 0, sizeof(a));
   a.topo = c->topo;
@@ -192,9 +203,20 @@ hetcclResult_t run_op(hetcclComm_t c, int op, const void* const* sends, void* co
   }
   int nch_max = c->nch_max;
   if (c->kind == KIND_MUX) {
-    int cap = max_coresident(op, dt, red);
+    int cap = max_coresident(oneshot ? OP_ALLREDUCE_ONESHOT : op, dt, red);
     if (cap < nlocal) return fail(c, hetcclInternalError, "device cannot co-schedule %d ranks", nlocal);
     nch_max = std::min(nch_max, cap / nlocal);
+  }
+  if (oneshot) {  // NEXT-3: one round trip; ~8 KiB of every rank's buffer per channel
+    a.op = OP_ALLREDUCE_ONESHOT;
+    a.count = count;
+    a.nch = (int)std::max<size_t>(1, std::min<size_t>((size_t)nch_max, (count * (size_t)es + 8191) / 8192));
+    a.os_off = scratch_slots_bytes(c);
+    a.os_stride = c->os_stride;
+    a.err = c->err;
+    a.timeout_ns = c->timeout_ns;
+    CUDA_TRY(c, launch_collective(a, nlocal, dt, red, c->kind == KIND_MUX, stream));
+    return hetcclSuccess;
   }
   const size_t slot_elems = c->slot_bytes / (size_t)es;
   Geometry geo = make_geometry(c->topo, op, count, es, nch_max, slot_elems);
@@ -307,6 +329,7 @@ hetcclResult_t hetccl_comm_export(hetcclComm_t c, void* blob, size_t* blob_bytes
   b.nch_max = c->nch_max;
   b.ws = c->ws;
   b.nslots = c->nslots;
+  b.os_bytes = c->os_bytes;
   DevGuard g(c->device);
   CUDA_TRY(c, cudaIpcGetMemHandle(&b.handle, c->local[0]));
   memset(blob, 0, HETCCL_BLOB_BYTES);
@@ -329,7 +352,8 @@ hetcclResult_t hetccl_comm_connect(hetcclComm_t c, const void* blobs, size_t blo
       return fail(c, hetcclInvalidUsage, "blob %d is not a hetccl blob for rank %d of %d", r, r, c->n);
     if (memcmp(b.map, c->map, sizeof(int) * c->n) != 0)
       return fail(c, hetcclInvalidUsage, "rank %d passed a different rank_to_domain map", r);
-    if (b.slot_bytes != c->slot_bytes || b.nch_max != c->nch_max || b.ws != c->ws || b.nslots != c->nslots)
+    if (b.slot_bytes != c->slot_bytes || b.nch_max != c->nch_max || b.ws != c->ws || b.nslots != c->nslots ||
+        b.os_bytes != c->os_bytes)
       return fail(c, hetcclInvalidUsage, "rank %d has different HETCCL_SLOT_KB/NCHANNELS/WS/NSLOTS", r);
     if (r == c->rank) continue;
     void* p = nullptr;
@@ -407,7 +431,7 @@ hetcclResult_t hetccl_comm_init_mux(hetcclComm_t* comm, int nranks, const int* r
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cuda_device);
     c->nch_max = std::max(1, std::min(c->nch_max, sms / nranks));
-    c->alloc_bytes = kFlagsReserve + (size_t)c->nch_max * c->nslots * c->slot_bytes;
+    c->alloc_bytes = alloc_bytes_for(c);
   }
   cudaError_t e = cudaSuccess;
   for (int r = 0; r < nranks && e == cudaSuccess; r++) e = alloc_region(c->alloc_bytes, &c->local[r]);

@@ -16,6 +16,7 @@ SPLITS = ["1+1", "2+2", "1+3", "1+1+2", "4+4", "2+6", "2+2+4", "8", "interleaved
 @pytest.fixture(autouse=True)
 def _env(monkeypatch):
     monkeypatch.setenv("HETCCL_TIMEOUT_S", "10")
+    monkeypatch.setenv("HETCCL_ONESHOT_KB", "0")  # these tests cover the hierarchical pipeline (test_gpu_oneshot.py the rest)
 
 
 def _hc():

@@ -15,6 +15,7 @@ pytestmark = pytest.mark.gpu
 @pytest.fixture(autouse=True)
 def _env(monkeypatch):
     monkeypatch.setenv("HETCCL_TIMEOUT_S", "10")
+    monkeypatch.setenv("HETCCL_ONESHOT_KB", "0")  # these tests cover the hierarchical pipeline (test_gpu_oneshot.py the rest)
 
 
 def _hc():
