@@ -29,7 +29,7 @@ struct hetcclComm {
   int n = 0, rank = 0, device = 0;
   int map[kMaxRanks] = {0};
   Topo topo{};
-  int nch_max = 128;
+  int nch_max = 148;
   size_t slot_bytes = 0;
   size_t alloc_bytes = 0;
   char* local[kMaxRanks] = {nullptr};    // allocations owned by this comm (mux: one per rank)
@@ -96,7 +96,7 @@ size_t alloc_bytes_for(const hetcclComm* c) {
 }
 
 void read_env(hetcclComm* c) {
-  c->nch_max = (int)std::max(1L, std::min((long)kMaxChannels, env_long("HETCCL_NCHANNELS", 128)));
+  c->nch_max = (int)std::max(1L, std::min((long)kMaxChannels, env_long("HETCCL_NCHANNELS", 148)));
   // scratch slot: HETCCL_SLOT_KB, else sized from this map so every op's default tile fits
   const long slot_kb = env_long("HETCCL_SLOT_KB", 0);
   c->slot_bytes = slot_kb > 0 ? (size_t)std::max(64L, slot_kb) * 1024

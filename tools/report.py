@@ -9,7 +9,8 @@
                 stream), wall time per step vs NCCL
 * c5          : Llama-7B gradients (6,738,415,616 elements, 13.5 GB bf16 per rank) in 256 MiB buckets
 Times: CUDA events on the launching stream, max over ranks (R16). busBW per R15. Parity: each
-measured buffer is checked bitwise against the oracle on sampled windows (tests/ owns full parity).
+measured AR/RS buffer passes DESIGN.md R7's gate vs an fp64 sum on sampled windows (tests/ owns bitwise
+parity against the oracle); AG/Broadcast results are compared bitwise with NCCL's.
 """
 import argparse
 import json
@@ -37,8 +38,8 @@ def main():
     import torch
     import torch.distributed as dist
     import paper_2601_22585_b200 as hc
-    import oracle
     import synth
+    from bench import fp64_gate
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -96,9 +97,8 @@ def main():
         for st in (0, max(0, count // 2 - W // 2), max(0, count - W)):
             w = min(W, count - st)
             xs = [synth.normal(seed, r, w, "bf16", start=st) for r in range(world)]
-            want = oracle.allreduce(xs, m, "bf16", "sum")
             got = y[st:st + w].cpu().view(torch.int16).numpy().view(np.uint16)
-            ok &= bool(np.array_equal(got, want))
+            ok &= fp64_gate(got, xs)
         t = torch.tensor([1 if ok else 0], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MIN)
         return bool(t.item())
@@ -121,7 +121,7 @@ def main():
         emit({"row": "allreduce", "split": name, "map": m, "n": world, "bytes": S, "dtype": "bf16", "ms": round(t * 1e3, 4),
               "algbw": round(alg, 2), "busbw": round(bus, 2), "nccl_busbw": round(nbus, 2),
               "vs_nccl": round(bus / nbus, 4), "busbw_over_900": round(bus / 900, 4),
-              "link_util_770": round(busiest / t / 1e9 / 770, 4), "parity_bitwise": ok})
+              "link_util_770": round(busiest / t / 1e9 / 770, 4), "r7_gate": ok})
         del x, y, z
 
     if args.what == "ar_sweep":
@@ -145,18 +145,18 @@ def main():
             y = torch.empty(R, dtype=torch.bfloat16, device="cuda")
             t = timed(lambda: hc.reduce_scatter(x, y, c), args.iters)
             W = 2048
-            xs = [synth.normal(3, r, count, "bf16") for r in range(world)] if rank == 0 else None
             ok = True
-            if rank == 0:
-                want = oracle.reduce_scatter([v[:] for v in xs], m, "bf16", "sum")[0]
+            if rank == 0:  # my block = elements [0, R) of every rank's input
                 got = y.cpu().view(torch.int16).numpy().view(np.uint16)
-                ok = bool(np.array_equal(got[:W], want[:W]) and np.array_equal(got[-W:], want[-W:]))
+                for st in (0, R - W):
+                    xs = [synth.normal(3, r, W, "bf16", start=st) for r in range(world)]
+                    ok &= fp64_gate(got[st:st + W], xs)
             yn = torch.empty_like(y)
             tn = timed(lambda: dist.reduce_scatter_tensor(yn, x), args.iters)
             f = (world - 1) / world
             emit({"row": "reduce_scatter", "split": name, "n": world, "bytes": S, "ms": round(t * 1e3, 4),
                   "busbw": round(S / t / 1e9 * f, 2), "nccl_busbw": round(S / tn / 1e9 * f, 2),
-                  "vs_nccl": round(tn / t, 4), "parity_bitwise_rank0": ok})
+                  "vs_nccl": round(tn / t, 4), "r7_gate_rank0": ok})
             # all-gather
             xa = x[:R].contiguous()
             ya = torch.empty(count, dtype=torch.bfloat16, device="cuda")
@@ -215,7 +215,7 @@ def main():
         tn = timed(nstep, 3, warm=1)
         emit({"row": "c4_buckets_nccl", "split": "flat", "n": world, "buckets": len(sizes), "bytes": total * 2,
               "ms": round(tn * 1e3, 3), "eff_busbw": round(total * 2 / tn / 1e9 * 2 * (world - 1) / world, 2),
-              "hetccl_parity_bitwise": ok})
+              "hetccl_r7_gate": ok})
     elif args.what == "c5":
         name = DEFAULT[world]
         m = SPLITS[world][name]
