@@ -158,8 +158,8 @@ def fp64_gate(got_u16, xs_u16):
     F = np.stack([bf16_to_f64(x) for x in xs_u16])
     R, A, g = F.sum(0), np.abs(F).sum(0), bf16_to_f64(got_u16)
     ok = bool(np.all(np.abs(g - R) <= 1e-2 * A + 1e-30))
-    nrm = np.linalg.norm(R)
-    return ok and (nrm == 0 or np.linalg.norm(g - R) / nrm <= 1e-2)
+    nrm = float(np.linalg.norm(R))
+    return bool(ok and (nrm == 0.0 or float(np.linalg.norm(g - R)) / nrm <= 1e-2))
 
 
 def gate_windows(recv_dev_list, window_inputs, starts, W):
@@ -168,8 +168,8 @@ def gate_windows(recv_dev_list, window_inputs, starts, W):
     ok = True
     for st, xs in zip(starts, window_inputs):
         for y in recv_dev_list:
-            ok &= fp64_gate(y[st:st + W].cpu().view(torch.int16).numpy().view(np.uint16), xs)
-    return ok
+            ok = ok and fp64_gate(y[st:st + W].cpu().view(torch.int16).numpy().view(np.uint16), xs)
+    return bool(ok)
 
 
 # ---------------------------------------------------------------------------------- N = 1 (mux)

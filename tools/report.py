@@ -71,16 +71,33 @@ def main():
                 out.write(line + "\n")
                 out.flush()
 
-    def timed(fn, iters, warm=3, stream=None):
+    def timed(fn, iters, warm=3, stream=None, graph=False):
+        """Mean device time per call (CUDA events, max over ranks). graph=True captures the `iters` calls
+        in one CUDA graph first, so host launch overhead does not bound small messages."""
         s = stream or torch.cuda.current_stream()
         for _ in range(warm):
             fn()
         torch.cuda.synchronize()
+        g = None
+        if graph:
+            g = torch.cuda.CUDAGraph()
+            cs = torch.cuda.Stream()
+            cs.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(cs):
+                with torch.cuda.graph(g, stream=cs):
+                    for _ in range(iters):
+                        fn()
+            torch.cuda.synchronize()
+            g.replay()
+            torch.cuda.synchronize()
         dist.barrier()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(s)
-        for _ in range(iters):
-            fn()
+        if g is not None:
+            g.replay()
+        else:
+            for _ in range(iters):
+                fn()
         b.record(s)
         torch.cuda.synchronize()
         t = torch.tensor([a.elapsed_time(b) / iters], device="cuda")
@@ -110,10 +127,13 @@ def main():
         y = torch.empty_like(x)
         c = comm_for(name, m)
         it = iters or (args.iters if mib <= 256 else max(3, args.iters // 4))
-        t = timed(lambda: hc.allreduce(x, y, c), it)
+        graph = mib <= 16  # launch-latency regime: time CUDA-graph replays (both libraries)
+        if graph:
+            it = 50
+        t = timed(lambda: hc.allreduce(x, y, c), it, graph=graph)
         ok = parity_ar(y, seed, count, m)
         z = x.clone()
-        tn = timed(lambda: dist.all_reduce(z), it)
+        tn = timed(lambda: dist.all_reduce(z), it, graph=graph)
         alg = S / t / 1e9
         bus = alg * 2 * (world - 1) / world
         nbus = S / tn / 1e9 * 2 * (world - 1) / world
@@ -121,7 +141,7 @@ def main():
         emit({"row": "allreduce", "split": name, "map": m, "n": world, "bytes": S, "dtype": "bf16", "ms": round(t * 1e3, 4),
               "algbw": round(alg, 2), "busbw": round(bus, 2), "nccl_busbw": round(nbus, 2),
               "vs_nccl": round(bus / nbus, 4), "busbw_over_900": round(bus / 900, 4),
-              "link_util_770": round(busiest / t / 1e9 / 770, 4), "r7_gate": ok})
+              "link_util_770": round(busiest / t / 1e9 / 770, 4), "r7_gate": ok, "cuda_graph": graph})
         del x, y, z
 
     if args.what == "ar_sweep":
