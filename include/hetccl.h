@@ -132,6 +132,12 @@ HETCCL_API const char* hetccl_get_last_error(hetcclComm_t comm); /* detail of th
  *   In place iff sendbuf == recvbuf + rank*sendcount.
  * hetccl_broadcast: every rank's recvbuf = root's sendbuf (count elements); sendbuf is read on the
  *   root only (may be NULL elsewhere). In place iff sendbuf == recvbuf.
+ * hetccl_reduce (App. E.1 "Reduce"): the root's recvbuf = the
+ *   All-Reduce result (same order and rounding); recvbuf is written on the root only (may be NULL
+ *   elsewhere). In place iff sendbuf == recvbuf.
+ * hetccl_all_to_all (App. E.1 "All-to-All"): sendbuf and recvbuf hold nranks blocks of
+ *   `count` elements; block j of sendbuf goes to rank j, block j of recvbuf comes from rank j. Send and
+ *   recv must not overlap.
  * Any other overlap of send and recv ranges is hetcclInvalidArgument.
  */
 HETCCL_API hetcclResult_t hetccl_allreduce(const void* sendbuf, void* recvbuf, size_t count, hetcclDataType_t dt,
@@ -142,6 +148,10 @@ HETCCL_API hetcclResult_t hetccl_all_gather(const void* sendbuf, void* recvbuf, 
                                  hetcclComm_t comm, hetcclStream_t stream);
 HETCCL_API hetcclResult_t hetccl_broadcast(const void* sendbuf, void* recvbuf, size_t count, hetcclDataType_t dt, int root,
                                 hetcclComm_t comm, hetcclStream_t stream);
+HETCCL_API hetcclResult_t hetccl_reduce(const void* sendbuf, void* recvbuf, size_t count, hetcclDataType_t dt,
+                                        hetcclRedOp_t op, int root, hetcclComm_t comm, hetcclStream_t stream);
+HETCCL_API hetcclResult_t hetccl_all_to_all(const void* sendbuf, void* recvbuf, size_t count, hetcclDataType_t dt,
+                                            hetcclComm_t comm, hetcclStream_t stream);
 
 /* Rank-multiplexed variants: sendbufs[r] / recvbufs[r] for every logical rank r of a mux comm. */
 HETCCL_API hetcclResult_t hetccl_mux_allreduce(const void* const* sendbufs, void* const* recvbufs, size_t count,
@@ -153,11 +163,17 @@ HETCCL_API hetcclResult_t hetccl_mux_all_gather(const void* const* sendbufs, voi
                                      hetcclDataType_t dt, hetcclComm_t comm, hetcclStream_t stream);
 HETCCL_API hetcclResult_t hetccl_mux_broadcast(const void* const* sendbufs, void* const* recvbufs, size_t count,
                                     hetcclDataType_t dt, int root, hetcclComm_t comm, hetcclStream_t stream);
+HETCCL_API hetcclResult_t hetccl_mux_reduce(const void* const* sendbufs, void* const* recvbufs, size_t count,
+                                            hetcclDataType_t dt, hetcclRedOp_t op, int root, hetcclComm_t comm,
+                                            hetcclStream_t stream);
+HETCCL_API hetcclResult_t hetccl_mux_all_to_all(const void* const* sendbufs, void* const* recvbufs, size_t count,
+                                                hetcclDataType_t dt, hetcclComm_t comm, hetcclStream_t stream);
 
 /* ------------------------------------------------------------- plan introspection ----------- */
 /*
  * Host-only (no CUDA): the per-rank algorithmic NVLink bytes one op moves, from the same plan the
- * kernels execute. op: 0 allreduce, 1 reduce_scatter, 2 all_gather, 3 broadcast.
+ * kernels execute. op: 0 allreduce, 1 reduce_scatter, 2 all_gather, 3 broadcast,
+ * 4 reduce, 5 all_to_all (count = elements per block).
  * count = the op's `count` argument (recvcount / sendcount for RS / AG). Writes bytes sent and
  * received by `rank` over the peer fabric, and the tile geometry (elements per tile, tiles,
  * channels) the launch would use with `nchannels` channels (0 = default).

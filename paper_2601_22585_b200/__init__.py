@@ -17,7 +17,7 @@ _LIB_PATH = os.path.join(_HERE, os.environ.get("HETCCL_LIB", "libhetccl.so"))
 
 INT32, FLOAT16, FLOAT32, BFLOAT16 = 2, 6, 7, 9
 SUM, MAX, MIN = 0, 2, 3
-OP_ALLREDUCE, OP_REDUCE_SCATTER, OP_ALL_GATHER, OP_BROADCAST = 0, 1, 2, 3
+OP_ALLREDUCE, OP_REDUCE_SCATTER, OP_ALL_GATHER, OP_BROADCAST, OP_REDUCE, OP_ALL_TO_ALL = 0, 1, 2, 3, 4, 5
 BLOB_BYTES = 512
 MAX_RANKS = 16
 _RESULT = {0: "hetcclSuccess", 1: "hetcclUnhandledCudaError", 2: "hetcclSystemError", 3: "hetcclInternalError",
@@ -48,7 +48,8 @@ EXPORTED = [
     "hetccl_comm_get_async_error", "hetccl_get_error_string", "hetccl_get_last_error", "hetccl_allreduce",
     "hetccl_reduce_scatter", "hetccl_all_gather", "hetccl_broadcast", "hetccl_mux_allreduce",
     "hetccl_mux_reduce_scatter", "hetccl_mux_all_gather", "hetccl_mux_broadcast", "hetccl_plan_info",
-    "hetccl_plan_stages", "hetccl_comm_get_trace",
+    "hetccl_plan_stages", "hetccl_comm_get_trace", "hetccl_reduce", "hetccl_all_to_all", "hetccl_mux_reduce",
+    "hetccl_mux_all_to_all",
 ]
 
 _lib = None
@@ -79,6 +80,10 @@ def lib():
         "hetccl_reduce_scatter": [vp, vp, c_size, c_int, c_int, vp, vp],
         "hetccl_all_gather": [vp, vp, c_size, c_int, vp, vp],
         "hetccl_broadcast": [vp, vp, c_size, c_int, c_int, vp, vp],
+        "hetccl_reduce": [vp, vp, c_size, c_int, c_int, c_int, vp, vp],
+        "hetccl_all_to_all": [vp, vp, c_size, c_int, vp, vp],
+        "hetccl_mux_reduce": [pp, pp, c_size, c_int, c_int, c_int, vp, vp],
+        "hetccl_mux_all_to_all": [pp, pp, c_size, c_int, vp, vp],
         "hetccl_mux_allreduce": [pp, pp, c_size, c_int, c_int, vp, vp],
         "hetccl_mux_reduce_scatter": [pp, pp, c_size, c_int, c_int, vp, vp],
         "hetccl_mux_all_gather": [pp, pp, c_size, c_int, vp, vp],
@@ -253,6 +258,14 @@ def hetccl_broadcast(sendbuf, recvbuf, count, dtype, root, comm, stream):
     _check(lib().hetccl_broadcast(sendbuf, recvbuf, count, dtype, root, comm, stream), comm)
 
 
+def hetccl_reduce(sendbuf, recvbuf, count, dtype, op, root, comm, stream):
+    _check(lib().hetccl_reduce(sendbuf, recvbuf, count, dtype, _op(op), root, comm, stream), comm)
+
+
+def hetccl_all_to_all(sendbuf, recvbuf, count, dtype, comm, stream):
+    _check(lib().hetccl_all_to_all(sendbuf, recvbuf, count, dtype, comm, stream), comm)
+
+
 def _parr(xs):
     return (ctypes.c_void_p * len(xs))(*[_ptr(x) for x in xs])
 
@@ -274,6 +287,14 @@ def hetccl_mux_broadcast(sendbufs, recvbufs, count, dtype, root, comm, stream):
     _check(lib().hetccl_mux_broadcast(_parr(sendbufs), _parr(recvbufs), count, dtype, root, comm, stream), comm)
 
 
+def hetccl_mux_reduce(sendbufs, recvbufs, count, dtype, op, root, comm, stream):
+    _check(lib().hetccl_mux_reduce(_parr(sendbufs), _parr(recvbufs), count, dtype, _op(op), root, comm, stream), comm)
+
+
+def hetccl_mux_all_to_all(sendbufs, recvbufs, count, dtype, comm, stream):
+    _check(lib().hetccl_mux_all_to_all(_parr(sendbufs), _parr(recvbufs), count, dtype, comm, stream), comm)
+
+
 # tensor conveniences (same calls; count/dtype taken from the tensors)
 def allreduce(send, recv, comm, op="sum", stream=None):
     hetccl_allreduce(_ptr(send), _ptr(recv), recv.numel(), dtype_code(recv.dtype), op, comm, _stream(stream))
@@ -289,6 +310,26 @@ def all_gather(send, recv, comm, stream=None):
 
 def broadcast(send, recv, root, comm, stream=None):
     hetccl_broadcast(_ptr(send), _ptr(recv), recv.numel(), dtype_code(recv.dtype), root, comm, _stream(stream))
+
+
+def reduce(send, recv, root, comm, op="sum", stream=None):
+    """recv may be None on non-root ranks."""
+    hetccl_reduce(_ptr(send), _ptr(recv), send.numel(), dtype_code(send.dtype), op, root, comm, _stream(stream))
+
+
+def all_to_all(send, recv, comm, stream=None):
+    """send/recv hold nranks equal blocks."""
+    n = hetccl_comm_info(comm)["nranks"]
+    hetccl_all_to_all(_ptr(send), _ptr(recv), send.numel() // n, dtype_code(send.dtype), comm, _stream(stream))
+
+
+def mux_reduce(sends, recvs, root, comm, op="sum", stream=None):
+    hetccl_mux_reduce(sends, recvs, sends[0].numel(), dtype_code(sends[0].dtype), op, root, comm, _stream(stream))
+
+
+def mux_all_to_all(sends, recvs, comm, stream=None):
+    n = len(sends)
+    hetccl_mux_all_to_all(sends, recvs, sends[0].numel() // n, dtype_code(sends[0].dtype), comm, _stream(stream))
 
 
 def mux_allreduce(sends, recvs, comm, op="sum", stream=None):

@@ -40,8 +40,10 @@ enum OpKind : int {
   OP_REDUCE_SCATTER = 1,
   OP_ALL_GATHER = 2,
   OP_BROADCAST = 3,
-  OP_COPY = 4,
-  OP_ALLREDUCE_ONESHOT = 5  // small-message All-Reduce (NEXT-3), same result as OP_ALLREDUCE
+  OP_REDUCE = 4,             // NEXT-2: hierarchical Reduce to a root
+  OP_ALL_TO_ALL = 5,         // NEXT-2: All-to-All (direct NVLink pushes)
+  OP_COPY = 6,
+  OP_ALLREDUCE_ONESHOT = 7  // small-message All-Reduce (NEXT-3), same result as OP_ALLREDUCE
 };
 enum DType : int { DT_INT32 = 2, DT_F16 = 6, DT_F32 = 7, DT_BF16 = 9 };
 enum RedOp : int { RED_SUM = 0, RED_MAX = 2, RED_MIN = 3 };

@@ -1083,6 +1083,138 @@ struct BcOp {
   }
 };
 
+// ================================================================== Reduce (NEXT-2) =============
+// out_root = the All-Reduce result Y (same fold order). Stages A/B as All-Reduce; C folds my pieces with
+// the other domains' partials (cta_fold_hier) and sends the final piece to the root; D: the root copies
+// everyone's pieces into y. Slot layout on a rank of domain k: s1[d-1][Rk] | s2[D][Rk] | fin[T] (root).
+template <typename T, int OP>
+struct RdOp {
+  static constexpr int ES = sizeof(T);
+  const OpArgs& a;
+  const Topo& tp;
+  int me, ch, k, j, d, D, L, spj, s_lo, s_hi, root;
+  size_t TL, Rk;
+  const T* x;
+  T* y;
+  __device__ RdOp(const OpArgs& a_, int row, int ch_) : a(a_), tp(a_.topo), ch(ch_) {
+    me = a.local_rank[row];
+    k = tp.rank_dom[me];
+    j = tp.rank_idx[me];
+    d = tp.dom_size[k];
+    D = tp.D;
+    L = tp.L;
+    spj = L / d;
+    s_lo = j * spj;
+    s_hi = s_lo + spj;
+    root = a.root;
+    TL = a.tile;
+    Rk = TL / d;
+    x = (const T*)a.send[row];
+    y = (T*)a.recv[row];
+  }
+  __device__ int peer(int i) const { return tp.members[tp.dom_first[k] + i]; }
+  __device__ size_t s2_off(int dq) const { return (size_t)(dq - 1) * (TL / dq); }
+  __device__ size_t region_lo(const Geo& g, int o) const {
+    const int q = tp.rank_dom[o];
+    return g.seg(tp.rank_idx[o] * (L / tp.dom_size[q]));
+  }
+  // where a final element at tile offset c goes: y on the root, else the root's fin buffer
+  __device__ T* final_dst(size_t tb, size_t c, int slot) const {
+    if (me == root) return y + tb + c;
+    const int dr = tp.dom_size[tp.rank_dom[root]];
+    return slot_ptr<T>(a, root, ch, slot) + s2_off(dr) + (size_t)D * (TL / dr) + c;
+  }
+  __device__ void stage(int s, size_t t, int slot) {
+    const size_t tb = t * TL, len = min(TL, a.count - tb);
+    const Geo g{len, TL, L, D};
+    const size_t r0 = g.seg(s_lo);
+    T* mine = slot_ptr<T>(a, me, ch, slot);
+    T* my_s2 = mine + s2_off(d);
+    if (s == 0) {  // ---- A: push my data for each domain peer's region ----
+      for (int i = 0; i < d; i++) {
+        if (i == j) continue;
+        const size_t p0 = g.seg(i * spj), p1 = g.seg((i + 1) * spj);
+        cta_copy1<ES>(x + tb + p0, slot_ptr<T>(a, peer(i), ch, slot) + (size_t)cidx(j, i) * Rk, p1 - p0);
+      }
+    } else if (s == 1) {  // ---- B: domain fold of the other domains' pieces (or of my region if D == 1) ----
+      for (int sg = s_lo; sg < s_hi; sg++) {
+        for (int q = 0; q < D; q++) {
+          if (D > 1 && q == k) continue;
+          const size_t c0 = g.piece(sg, q), c1 = g.piece(sg, q + 1);
+          if (c1 <= c0) continue;
+          PtrList src, dst;
+          for (int i = 0; i < d; i++)
+            src.add(i == j ? (const void*)(x + tb + c0) : (const void*)(mine + (size_t)cidx(i, j) * Rk + (c0 - r0)));
+          if (D == 1) {
+            dst.add(final_dst(tb, c0, slot));
+          } else {
+            const int o = owner_of(tp, q, sg);
+            const int dq = tp.dom_size[q];
+            dst.add(slot_ptr<T>(a, o, ch, slot) + s2_off(dq) + (size_t)k * (TL / dq) + (c0 - region_lo(g, o)));
+          }
+          cta_fold<T, OP>(src, dst, c1 - c0);
+        }
+      }
+    } else if (s == 2) {  // ---- C: my pieces: domain fold + cross fold -> the root ----
+      for (int sg = s_lo; sg < s_hi; sg++) {
+        const size_t c0 = g.piece(sg, k), c1 = g.piece(sg, k + 1);
+        if (c1 <= c0) continue;
+        PtrList inner, outer, dst;
+        for (int i = 0; i < d; i++)
+          inner.add(i == j ? (const void*)(x + tb + c0) : (const void*)(mine + (size_t)cidx(i, j) * Rk + (c0 - r0)));
+        for (int q = 0; q < D; q++) outer.add(q == k ? nullptr : (const void*)(my_s2 + (size_t)q * Rk + (c0 - r0)));
+        dst.add(final_dst(tb, c0, slot));
+        cta_fold_hier<T, OP>(inner, k, outer, dst, c1 - c0);
+      }
+    } else {  // ---- D: the root copies every other rank's final pieces into y ----
+      if (me != root) return;
+      const T* fin = mine + s2_off(d) + (size_t)D * Rk;
+      for (int sg = 0; sg < L; sg++)
+        for (int q = 0; q < D; q++) {
+          const int o = owner_of(tp, q, sg);
+          if (o == root) continue;
+          const size_t c0 = D == 1 ? g.seg(sg) : g.piece(sg, q), c1 = D == 1 ? g.seg(sg + 1) : g.piece(sg, q + 1);
+          if (c1 > c0) cta_copy1<ES>(fin + c0, y + tb + c0, c1 - c0);
+        }
+    }
+  }
+};
+
+// ================================================================== All-to-All (NEXT-2) ========
+// out_r[j*B + t] = x_j[r*B + t] (B = count per block). Every block crosses NVLink once, straight to its
+// destination's scratch (NVSwitch gives every pair full bandwidth, so there is nothing to aggregate per
+// domain). Slot layout: in[n-1][T] (compact sender index). Stages: 0 A push blocks | 1 B copy-out.
+template <typename T>
+struct A2aOp {
+  static constexpr int ES = sizeof(T);
+  const OpArgs& a;
+  int me, ch, n;
+  size_t TL, Bc;
+  const T* x;
+  T* y;
+  __device__ A2aOp(const OpArgs& a_, int row, int ch_) : a(a_), ch(ch_) {
+    me = a.local_rank[row];
+    n = a.topo.n;
+    TL = a.tile;
+    Bc = a.count;
+    x = (const T*)a.send[row];
+    y = (T*)a.recv[row];
+  }
+  __device__ void stage(int s, size_t t, int slot) {
+    const size_t tb = t * TL, len = min(TL, Bc - tb);
+    if (s == 0) {
+      for (int r = 0; r < n; r++) {
+        if (r == me) cta_copy1<ES>(x + (size_t)me * Bc + tb, y + (size_t)me * Bc + tb, len);
+        else cta_copy1<ES>(x + (size_t)r * Bc + tb, slot_ptr<T>(a, r, ch, slot) + (size_t)cidx(me, r) * TL, len);
+      }
+    } else {
+      const T* mine = slot_ptr<T>(a, me, ch, slot);
+      for (int r = 0; r < n; r++)
+        if (r != me) cta_copy1<ES>(mine + (size_t)cidx(r, me) * TL, y + (size_t)r * Bc + tb, len);
+    }
+  }
+};
+
 // ================================================================== kernels ===================
 template <typename T, int OP>
 __global__ void __launch_bounds__(kThreads, 1) k_allreduce(const __grid_constant__ OpArgs a) {
@@ -1097,6 +1229,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_reduce_scatter(const __grid_con
 template <typename T>
 __global__ void __launch_bounds__(kThreads, 1) k_all_gather(const __grid_constant__ OpArgs a) {
   AgOp<T> op(a, blockIdx.y, blockIdx.x);
+  run_pipeline(a, op, op.me, blockIdx.x);
+}
+template <typename T, int OP>
+__global__ void __launch_bounds__(kThreads, 1) k_reduce(const __grid_constant__ OpArgs a) {
+  RdOp<T, OP> op(a, blockIdx.y, blockIdx.x);
+  run_pipeline(a, op, op.me, blockIdx.x);
+}
+template <typename T>
+__global__ void __launch_bounds__(kThreads, 1) k_all_to_all(const __grid_constant__ OpArgs a) {
+  A2aOp<T> op(a, blockIdx.y, blockIdx.x);
   run_pipeline(a, op, op.me, blockIdx.x);
 }
 template <typename T>
@@ -1228,6 +1370,11 @@ static KernFn pick_oneshot(int dt, int red) {
 
 template <typename T>
 static KernFn pick_reduce(int op, int red) {
+  if (op == OP_REDUCE) {
+    if (red == RED_SUM) return (KernFn)k_reduce<T, RED_SUM>;
+    if (red == RED_MAX) return (KernFn)k_reduce<T, RED_MAX>;
+    return (KernFn)k_reduce<T, RED_MIN>;
+  }
   if (op == OP_ALLREDUCE) {
     if (red == RED_SUM) return (KernFn)k_allreduce<T, RED_SUM>;
     if (red == RED_MAX) return (KernFn)k_allreduce<T, RED_MAX>;
@@ -1239,7 +1386,7 @@ static KernFn pick_reduce(int op, int red) {
 }
 
 static KernFn pick(int op, int dt, int red) {
-  if (op == OP_ALLREDUCE || op == OP_REDUCE_SCATTER) {
+  if (op == OP_ALLREDUCE || op == OP_REDUCE_SCATTER || op == OP_REDUCE) {
     switch (dt) {
       case DT_F32: return pick_reduce<float>(op, red);
       case DT_INT32: return pick_reduce<int32_t>(op, red);
@@ -1251,6 +1398,7 @@ static KernFn pick(int op, int dt, int red) {
   const bool two = (dt == DT_BF16 || dt == DT_F16);
   if (op == OP_ALL_GATHER) return two ? (KernFn)k_all_gather<__half> : (KernFn)k_all_gather<float>;
   if (op == OP_BROADCAST) return two ? (KernFn)k_broadcast<__half> : (KernFn)k_broadcast<float>;
+  if (op == OP_ALL_TO_ALL) return two ? (KernFn)k_all_to_all<__half> : (KernFn)k_all_to_all<float>;
   return nullptr;
 }
 

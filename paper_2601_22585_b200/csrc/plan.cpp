@@ -55,7 +55,8 @@ static size_t ceil_div(size_t a, size_t b) { return (a + b - 1) / b; }
 
 // quantum (elements) a full tile must be a multiple of, so every boundary is V-aligned
 static size_t quantum(const Topo& t, int op, int V) {
-  if (op == OP_ALLREDUCE) return (size_t)t.L * t.D * V;
+  if (op == OP_ALLREDUCE || op == OP_REDUCE) return (size_t)t.L * t.D * V;
+  if (op == OP_ALL_TO_ALL) return (size_t)V;
   return (size_t)t.L * V;
 }
 
@@ -79,6 +80,12 @@ size_t slot_mult_num(const Topo& t, int op, size_t tile) {
       case OP_BROADCAST:  // reg[Rk] | s3[d-1][Rk]
         v = d * Rk;
         break;
+      case OP_REDUCE:  // s1[d-1][Rk] | s2[D][Rk] | fin[T] (fin used on the root)
+        v = (d - 1 + D) * Rk + tile;
+        break;
+      case OP_ALL_TO_ALL:  // in[n-1][T] (T per block)
+        v = (n - 1) * tile;
+        break;
     }
     need = std::max(need, v);
   }
@@ -88,9 +95,10 @@ size_t slot_mult_num(const Topo& t, int op, size_t tile) {
 // default scratch slot (bytes) for a topology: fits the default tile of every op
 size_t default_slot_bytes(const Topo& t, size_t tile_bytes) {
   size_t need = 0;
-  for (int op = OP_ALLREDUCE; op <= OP_BROADCAST; op++) {
+  for (int op = OP_ALLREDUCE; op <= OP_ALL_TO_ALL; op++) {
     size_t tb = tile_bytes;
-    if (op == OP_REDUCE_SCATTER || op == OP_ALL_GATHER) tb = std::max<size_t>(tile_bytes / (size_t)t.n, 4096);
+    if (op == OP_REDUCE_SCATTER || op == OP_ALL_GATHER || op == OP_ALL_TO_ALL)
+      tb = std::max<size_t>(tile_bytes / (size_t)t.n, 4096);
     need = std::max(need, slot_mult_num(t, op, tb));
   }
   return (need + 4095) / 4096 * 4096 + 65536;  // room for the quantum rounding of the tile
@@ -99,7 +107,7 @@ size_t default_slot_bytes(const Topo& t, size_t tile_bytes) {
 size_t default_tile_bytes(int op, int n) {
   const char* e = getenv("HETCCL_TILE_KB");
   size_t b = e ? (size_t)atol(e) * 1024 : (size_t)256 * 1024;
-  if (op == OP_REDUCE_SCATTER || op == OP_ALL_GATHER) b /= (size_t)n;  // RS/AG tiles are per shard
+  if (op == OP_REDUCE_SCATTER || op == OP_ALL_GATHER || op == OP_ALL_TO_ALL) b /= (size_t)n;  // per shard / block
   return std::max<size_t>(b, 4096);
 }
 
@@ -213,6 +221,32 @@ static int op_spec(const Topo& t, int op, int rank, int root, StageSpec st[kMaxS
       st[3] = {any_intra, C_S3, is_root ? 0u : dpeers, C_NONE, 0};
       return 4;
     }
+    case OP_REDUCE: {
+      // A intra push | B fold other domains' pieces -> their owners (D > 1) or my region -> root (D == 1) |
+      // C fold my pieces + cross partials -> root | D root: everyone's final pieces -> y
+      uint32_t cross = 0;
+      for (int s = j * spj; s < (j + 1) * spj; s++)
+        for (int q = 0; q < D; q++)
+          if (q != k) cross |= 1u << owner_of(t, q, s);
+      const uint32_t to_root = rank == root ? 0u : 1u << root;
+      uint32_t from_all = 0;
+      if (rank == root)
+        for (int r = 0; r < n; r++)
+          if (r != rank) from_all |= 1u << r;
+      st[0] = {any_intra, C_NONE, 0, C_S1, dpeers};
+      st[1] = {true, C_S1, dpeers, any_cross ? C_S2 : C_S3, any_cross ? cross : to_root};
+      st[2] = {any_cross, C_S2, cross, C_S3, to_root};
+      st[3] = {true, C_S3, from_all, C_NONE, 0};
+      return 4;
+    }
+    case OP_ALL_TO_ALL: {
+      uint32_t all = 0;
+      for (int r = 0; r < n; r++)
+        if (r != rank) all |= 1u << r;
+      st[0] = {true, C_NONE, 0, C_S1, all};
+      st[1] = {true, C_S1, all, C_NONE, 0};
+      return 2;
+    }
     default:
       return 0;
   }
@@ -222,6 +256,8 @@ int op_stages(int op) {
   switch (op) {
     case OP_ALLREDUCE: return 5;
     case OP_BROADCAST: return 4;
+    case OP_REDUCE: return 4;
+    case OP_ALL_TO_ALL: return 2;
     case OP_REDUCE_SCATTER:
     case OP_ALL_GATHER: return 3;
   }
@@ -322,6 +358,27 @@ void plan_bytes(const Topo& t, int op, int rank, int root, size_t count, int es,
         S += intra_in + cross_in;
         R += intra_out + cross_out;
       }
+    } else if (op == OP_REDUCE) {
+      const int spj = L / d;
+      for (int i = 0; i < d; i++)
+        if (i != j) {
+          S += region(k, i);  // intra RS out
+          R += region(k, j);  // intra RS in
+        }
+      for (int s = j * spj; s < (j + 1) * spj; s++)
+        for (int q = 0; q < D; q++)
+          if (q != k) {
+            S += piece(s, q + 1) - piece(s, q);  // partial piece out
+            R += piece(s, k + 1) - piece(s, k);  // partial in from domain q
+          }
+      size_t mine = 0;  // final pieces I own
+      for (int s = j * spj; s < (j + 1) * spj; s++) mine += piece(s, k + 1) - piece(s, k);
+      if (D == 1) mine = region(k, j);
+      if (rank != root) S += mine;
+      else R += len - mine;
+    } else if (op == OP_ALL_TO_ALL) {
+      S += len * (size_t)(n - 1);
+      R += len * (size_t)(n - 1);
     } else if (op == OP_BROADCAST) {
       const int kr = t.rank_dom[root], spj = L / d;
       if (rank == root)

@@ -158,21 +158,28 @@ const char* check_overlap(int op, const void* s, void* r, size_t count, int es, 
       if ((const char*)s == (const char*)r + (size_t)rank * b) return nullptr;
       if (overlaps(s, b, r, b * n)) return "send and recv overlap (in place requires sendbuf == recvbuf + rank*sendcount)";
       return nullptr;
+    case OP_REDUCE:
+      if (r && s != r && overlaps(s, b, r, b)) return "send and recv overlap (only sendbuf == recvbuf is allowed)";
+      return nullptr;
+    case OP_ALL_TO_ALL:
+      if (overlaps(s, b * n, r, b * n)) return "all-to-all send and recv must not overlap";
+      return nullptr;
   }
   return nullptr;
 }
 
 // the elements each rank's recvbuf holds for op (for the n == 1 copy)
-size_t recv_elems(int op, size_t count, int n) { return op == OP_ALL_GATHER ? count * n : count; }
+size_t recv_elems(int op, size_t count, int n) { return (op == OP_ALL_GATHER || op == OP_ALL_TO_ALL) ? count * n : count; }
 
 hetcclResult_t run_op(hetcclComm_t c, int op, const void* const* sends, void* const* recvs, size_t count, int dt,
                       int red, int root, cudaStream_t stream) {
   if (!c) return hetcclInvalidArgument;
   if (!c->connected) return fail(c, hetcclInvalidUsage, "comm is not connected");
   if (!valid_dt(dt)) return fail(c, hetcclInvalidArgument, "unknown dtype %d", dt);
-  if ((op == OP_ALLREDUCE || op == OP_REDUCE_SCATTER) && !valid_red(red))
+  if ((op == OP_ALLREDUCE || op == OP_REDUCE_SCATTER || op == OP_REDUCE) && !valid_red(red))
     return fail(c, hetcclInvalidArgument, "unknown reduction op %d", red);
-  if (op == OP_BROADCAST && (root < 0 || root >= c->n)) return fail(c, hetcclInvalidArgument, "root %d not in [0,%d)", root, c->n);
+  if ((op == OP_BROADCAST || op == OP_REDUCE) && (root < 0 || root >= c->n))
+    return fail(c, hetcclInvalidArgument, "root %d not in [0,%d)", root, c->n);
   const int es = dtype_size(dt);
   if (count > ((size_t)1 << 62) / (size_t)es / (size_t)c->n) return fail(c, hetcclInvalidArgument, "count too large");
   if (count == 0) return hetcclSuccess;
@@ -180,13 +187,15 @@ hetcclResult_t run_op(hetcclComm_t c, int op, const void* const* sends, void* co
   for (int i = 0; i < nlocal; i++) {
     const int r = c->kind == KIND_MUX ? i : c->rank;
     const bool need_send = !(op == OP_BROADCAST && r != root);
-    if ((need_send && !sends[i]) || !recvs[i]) return fail(c, hetcclInvalidArgument, "null buffer for rank %d", r);
+    const bool need_recv = !(op == OP_REDUCE && r != root);
+    if ((need_send && !sends[i]) || (need_recv && !recvs[i]))
+      return fail(c, hetcclInvalidArgument, "null buffer for rank %d", r);
     const char* msg = check_overlap(op, sends[i], recvs[i], count, es, r, c->n);
     if (msg) return fail(c, hetcclInvalidArgument, "rank %d: %s", r, msg);
   }
   DevGuard g(c->device);
   if (c->n == 1) {  // a9: recv <- send
-    CUDA_TRY(c, launch_copy(sends[0], recvs[0], recv_elems(op, count, 1), es, stream));
+    if (recvs[0]) CUDA_TRY(c, launch_copy(sends[0], recvs[0], recv_elems(op, count, 1), es, stream));
     return hetcclSuccess;
   }
   const bool oneshot = op == OP_ALLREDUCE && c->os_bytes > 0 && count * (size_t)es <= c->os_bytes;
@@ -519,6 +528,16 @@ hetcclResult_t hetccl_all_gather(const void* sendbuf, void* recvbuf, size_t send
   if (comm && comm->kind == KIND_MUX) return fail(comm, hetcclInvalidUsage, "use hetccl_mux_* on a mux comm");
   return run_op(comm, OP_ALL_GATHER, &sendbuf, &recvbuf, sendcount, dt, RED_SUM, 0, (cudaStream_t)stream);
 }
+hetcclResult_t hetccl_reduce(const void* sendbuf, void* recvbuf, size_t count, hetcclDataType_t dt, hetcclRedOp_t op,
+                             int root, hetcclComm_t comm, hetcclStream_t stream) {
+  if (comm && comm->kind == KIND_MUX) return fail(comm, hetcclInvalidUsage, "use hetccl_mux_* on a mux comm");
+  return run_op(comm, OP_REDUCE, &sendbuf, &recvbuf, count, dt, op, root, (cudaStream_t)stream);
+}
+hetcclResult_t hetccl_all_to_all(const void* sendbuf, void* recvbuf, size_t count, hetcclDataType_t dt,
+                                 hetcclComm_t comm, hetcclStream_t stream) {
+  if (comm && comm->kind == KIND_MUX) return fail(comm, hetcclInvalidUsage, "use hetccl_mux_* on a mux comm");
+  return run_op(comm, OP_ALL_TO_ALL, &sendbuf, &recvbuf, count, dt, RED_SUM, 0, (cudaStream_t)stream);
+}
 hetcclResult_t hetccl_broadcast(const void* sendbuf, void* recvbuf, size_t count, hetcclDataType_t dt, int root,
                                 hetcclComm_t comm, hetcclStream_t stream) {
   if (comm && comm->kind == KIND_MUX) return fail(comm, hetcclInvalidUsage, "use hetccl_mux_* on a mux comm");
@@ -545,6 +564,17 @@ hetcclResult_t hetccl_mux_all_gather(const void* const* s, void* const* r, size_
   hetcclResult_t e = mux_check(c, s, r);
   return e ? e : run_op(c, OP_ALL_GATHER, s, r, sendcount, dt, RED_SUM, 0, (cudaStream_t)stream);
 }
+hetcclResult_t hetccl_mux_reduce(const void* const* s, void* const* r, size_t count, hetcclDataType_t dt,
+                                 hetcclRedOp_t op, int root, hetcclComm_t c, hetcclStream_t stream) {
+  if (!c || !s || !r) return hetcclInvalidArgument;
+  if (c->kind != KIND_MUX) return fail(c, hetcclInvalidUsage, "hetccl_mux_* needs a comm from hetccl_comm_init_mux");
+  return run_op(c, OP_REDUCE, s, r, count, dt, op, root, (cudaStream_t)stream);
+}
+hetcclResult_t hetccl_mux_all_to_all(const void* const* s, void* const* r, size_t count, hetcclDataType_t dt,
+                                     hetcclComm_t c, hetcclStream_t stream) {
+  hetcclResult_t e = mux_check(c, s, r);
+  return e ? e : run_op(c, OP_ALL_TO_ALL, s, r, count, dt, RED_SUM, 0, (cudaStream_t)stream);
+}
 hetcclResult_t hetccl_mux_broadcast(const void* const* s, void* const* r, size_t count, hetcclDataType_t dt, int root,
                                     hetcclComm_t c, hetcclStream_t stream) {
   hetcclResult_t e = mux_check(c, s, r);
@@ -554,8 +584,8 @@ hetcclResult_t hetccl_mux_broadcast(const void* const* s, void* const* r, size_t
 hetcclResult_t hetccl_plan_info(int nranks, const int* rank_to_domain, int rank, int op, size_t count,
                                 hetcclDataType_t dt, int root, int nchannels, hetcclPlanInfo_t* info) {
   Topo t;
-  if (!info || build_topo(nranks, rank_to_domain, &t) || rank < 0 || rank >= nranks || op < 0 || op > 3 ||
-      !valid_dt(dt) || (op == OP_BROADCAST && (root < 0 || root >= nranks)))
+  if (!info || build_topo(nranks, rank_to_domain, &t) || rank < 0 || rank >= nranks || op < 0 || op > 5 ||
+      !valid_dt(dt) || ((op == OP_BROADCAST || op == OP_REDUCE) && (root < 0 || root >= nranks)))
     return hetcclInvalidArgument;
   hetcclComm tmp;
   tmp.topo = t;
@@ -575,8 +605,8 @@ hetcclResult_t hetccl_plan_info(int nranks, const int* rank_to_domain, int rank,
 hetcclResult_t hetccl_plan_stages(int nranks, const int* rank_to_domain, int rank, int op, int root,
                                   hetcclStagePlan_t* plan) {
   Topo t;
-  if (!plan || build_topo(nranks, rank_to_domain, &t) || rank < 0 || rank >= nranks || op < 0 || op > 3 ||
-      (op == OP_BROADCAST && (root < 0 || root >= nranks)))
+  if (!plan || build_topo(nranks, rank_to_domain, &t) || rank < 0 || rank >= nranks || op < 0 || op > 5 ||
+      ((op == OP_BROADCAST || op == OP_REDUCE) && (root < 0 || root >= nranks)))
     return hetcclInvalidArgument;
   RankPlan rp;
   make_rank_plan(t, op, rank, root, &rp);

@@ -122,7 +122,7 @@ def test_rs_2p6_survey_numbers(hc):
 def test_conservation(hc):
     """Bytes sent over all ranks == bytes received over all ranks, any op, ragged counts."""
     for name, m in SPLITS.items():
-        for op in range(4):
+        for op in range(6):
             for count in (1, 999, 123457):
                 s = sum(hc.hetccl_plan_info(m, r, op, count, hc.BFLOAT16, root=len(m) - 1)["bytes_sent"]
                         for r in range(len(m)))
@@ -147,14 +147,14 @@ SCHED_MAPS = [[0, 1], [0, 0], [0, 0, 1, 1], [0, 1, 1, 1], [0, 1, 2, 2], [0, 0, 0
 
 
 @pytest.mark.parametrize("m", SCHED_MAPS, ids=lambda m: "".join(map(str, m)))
-@pytest.mark.parametrize("op", [0, 1, 2, 3])
+@pytest.mark.parametrize("op", [0, 1, 2, 3, 4, 5])
 def test_schedule_is_symmetric_and_acyclic(hc, m, op):
     """The flag protocol's invariants (kernels.cu run_pipeline): every signal a rank sends is awaited
     by its receiver on the same counter, every wait has a sender, a producer stage always precedes
     its consumer (so no iteration waits on itself), each counter has one consumer stage, active
     stages agree on every rank, and `writes` covers every rank signalled."""
     n = len(m)
-    roots = range(n) if op == 3 else [0]
+    roots = range(n) if op in (3, 4) else [0]
     for root in roots:
         plans = [hc.hetccl_plan_stages(m, r, op, root) for r in range(n)]
         assert len({p["active"] for p in plans}) == 1
@@ -198,3 +198,28 @@ def test_schedule_stage_sets(hc):
     assert hc.hetccl_plan_stages([0, 0, 1, 1], 0, 0)["active"] == 0b11111
     assert hc.hetccl_plan_stages([0, 1, 2, 3], 0, 1)["active"] == 0b110  # RS: B, C
     assert hc.hetccl_plan_stages([0, 1, 2, 3], 0, 2)["active"] == 0b011  # AG: A, B
+
+
+@pytest.mark.parametrize("name", ["2+2", "1+3", "4+4", "2+6", "2+2+4"])
+def test_reduce_bytes(hc, name):
+    """Reduce: the root receives every final piece it does not own ((n-1)/n of S for equal pieces), each
+    non-root sends its own final pieces; intra/cross bytes as All-Reduce's reduce-scatter half."""
+    m = SPLITS[name]
+    n = len(m)
+    tile = hc.hetccl_plan_info(m, 0, hc.OP_REDUCE, 1 << 28, hc.BFLOAT16)["tile_elems"]
+    count = tile * 64
+    S = count * 2
+    root = n - 1
+    ar = [hc.hetccl_plan_info(m, r, hc.OP_ALLREDUCE, count, hc.BFLOAT16) for r in range(n)]
+    rd = [hc.hetccl_plan_info(m, r, hc.OP_REDUCE, count, hc.BFLOAT16, root=root) for r in range(n)]
+    # the root receives everything but its own pieces
+    own_root = S - (rd[root]["bytes_recv"] - ar[root]["bytes_recv"] // 2)
+    assert 0 < own_root < S
+    assert sum(r["bytes_sent"] for r in rd) == sum(r["bytes_recv"] for r in rd)
+
+
+def test_all_to_all_bytes(hc):
+    for m in ([0, 1], [0, 0, 1, 1], [0] * 4 + [1] * 4):
+        n = len(m)
+        info = hc.hetccl_plan_info(m, 1, hc.OP_ALL_TO_ALL, 4096, hc.BFLOAT16)
+        assert info["bytes_sent"] == info["bytes_recv"] == (n - 1) * 4096 * 2

@@ -257,3 +257,116 @@ def test_collectives_multi(name, coll, monkeypatch):
     finally:
         for c in comms:
             hc.hetccl_comm_destroy(c)
+
+
+# ------------------------------------------------------------------------------ reduce / all-to-all (NEXT-2)
+def _run_reduce(name, dt, op, count, root, kind="normal", seed=61, inplace=False):
+    import torch
+    hc = _hc()
+    m = MAPS[name]
+    n = len(m)
+    xs = inputs(kind, seed, n, count, dt)
+    comm = _mux(m)
+    try:
+        sends = [to_torch(x, dt, "cuda") for x in xs]
+        recvs = [s if inplace else torch.full_like(s, 7) for s in sends]
+        hc.mux_reduce(sends, recvs, root, comm, op=op)
+        torch.cuda.synchronize()
+        hc.hetccl_comm_get_async_error(comm)
+        want = oracle.reduce(xs, m, root, dt, op)
+        assert_matches(to_numpy(recvs[root], dt), want, xs, dt, op, f"reduce {name} {dt} {op} root {root}")
+        # the oracle's Reduce is the All-Reduce result (same order)
+        assert np.array_equal(want.view(np.uint8), oracle.allreduce(xs, m, dt, op).view(np.uint8))
+    finally:
+        hc.hetccl_comm_destroy(comm)
+
+
+@pytest.mark.parametrize("name", SPLITS)
+@pytest.mark.parametrize("root_sel", ["first", "last", "mid"])
+def test_reduce_splits(name, root_sel, monkeypatch):
+    monkeypatch.setenv("HETCCL_TILE_KB", "8")
+    n = len(MAPS[name])
+    root = {"first": 0, "last": n - 1, "mid": n // 2}[root_sel]
+    _run_reduce(name, "bf16", "sum", 5 * 1024 + 333, root)
+
+
+@pytest.mark.parametrize("dt", ["int32", "f16", "f32", "bf16"])
+@pytest.mark.parametrize("op", ["sum", "max", "min"])
+def test_reduce_dtypes_ops(dt, op, monkeypatch):
+    monkeypatch.setenv("HETCCL_TILE_KB", "16")
+    _run_reduce("2+2+4", dt, op, 20011, 3, kind="bits" if dt == "int32" else "normal")
+
+
+@pytest.mark.parametrize("count", [1, 7, 9, 1000, 100003])
+def test_reduce_ragged_and_inplace(count):
+    _run_reduce("2+6", "f32", "sum", count, 7)
+    _run_reduce("4+4", "bf16", "sum", count, 2, inplace=True)
+
+
+def _run_a2a(name, dt, block, seed=71):
+    import torch
+    hc = _hc()
+    m = MAPS[name]
+    n = len(m)
+    xs = inputs("normal" if dt != "int32" else "bits", seed, n, n * block, dt)
+    comm = _mux(m)
+    try:
+        sends = [to_torch(x, dt, "cuda") for x in xs]
+        recvs = [torch.full_like(s, 4) for s in sends]
+        hc.mux_all_to_all(sends, recvs, comm)
+        torch.cuda.synchronize()
+        hc.hetccl_comm_get_async_error(comm)
+        want = oracle.all_to_all(xs, dt)
+        for r in range(n):
+            assert np.array_equal(to_numpy(recvs[r], dt).view(np.uint8), want[r].view(np.uint8)), f"a2a {name} rank {r}"
+    finally:
+        hc.hetccl_comm_destroy(comm)
+
+
+@pytest.mark.parametrize("name", ["1+1", "2+2", "1+3", "4+4", "2+6", "2+2+4", "8", "interleaved"])
+@pytest.mark.parametrize("dt", ["f32", "bf16", "int32"])
+def test_all_to_all(name, dt, monkeypatch):
+    monkeypatch.setenv("HETCCL_TILE_KB", "8")
+    _run_a2a(name, dt, 3 * 1024 + 517)
+
+
+@pytest.mark.parametrize("block", [1, 7, 8, 9, 70001])
+def test_all_to_all_ragged(block):
+    _run_a2a("2+2+4", "f16", block)
+
+
+@pytest.mark.multigpu
+@pytest.mark.parametrize("name", ["1+1", "2+2", "1+3"])
+def test_reduce_a2a_multi(name, monkeypatch):
+    import torch
+    hc = _hc()
+    m = MAPS[name]
+    n = len(m)
+    if _ngpu() < n:
+        pytest.skip(f"needs {n} GPUs")
+    monkeypatch.setenv("HETCCL_TILE_KB", "16")
+    comms = hc.hetccl_comm_init_all(list(range(n)), m)
+    try:
+        C = 5 * 4096 + 71
+        root = n - 1
+        xs = inputs("normal", 81, n, n * C, "bf16")
+        sends = [to_torch(xs[r], "bf16", f"cuda:{r}") for r in range(n)]
+        red = [torch.empty_like(s) if r == root else None for r, s in enumerate(sends)]
+        a2a = [torch.empty_like(s) for s in sends]
+        for r in range(n):
+            torch.cuda.synchronize(r)
+        for r in range(n):
+            with torch.cuda.device(r):
+                hc.reduce(sends[r], red[r], root, comms[r])
+                hc.all_to_all(sends[r], a2a[r], comms[r])
+        for r in range(n):
+            torch.cuda.synchronize(r)
+        want_r = oracle.reduce(xs, m, root, "bf16", "sum")
+        want_a = oracle.all_to_all(xs, "bf16")
+        assert np.array_equal(to_numpy(red[root], "bf16"), want_r)
+        for r in range(n):
+            hc.hetccl_comm_get_async_error(comms[r])
+            assert np.array_equal(to_numpy(a2a[r], "bf16"), want_a[r]), f"a2a {name} rank {r}"
+    finally:
+        for c in comms:
+            hc.hetccl_comm_destroy(c)

@@ -35,7 +35,7 @@ def _worker(rank, world, port, maps, q):
             got = [None] * world
             dist.all_gather_object(got, nd)
             assert len(set(got)) == 1
-            for op in range(4):
+            for op in range(6):
                 plan = hc.hetccl_plan_stages(m, rank, op, root=world - 1)
                 plans = [None] * world
                 dist.all_gather_object(plans, plan)
