@@ -136,7 +136,17 @@ Geometry make_geometry(const Topo& t, int op, size_t count, int es, int nch_max,
   }
   size_t target = std::max(q, floor_to(default_tile_bytes(op, t.n) / es, q));
   size_t tile = std::min(cap, target);
-  size_t per_ch = ceil_div(count, (size_t)nch_max);
+  // mid-size messages: shrink the tile (down to a floor) so every channel still gets a few tiles to
+  // pipeline, instead of one tile walking all stages serially (HETCCL_MIN_TILES, HETCCL_TILE_FLOOR_KB)
+  const char* e1 = getenv("HETCCL_MIN_TILES");
+  const char* e2 = getenv("HETCCL_TILE_FLOOR_KB");
+  const size_t min_tiles = std::max(1L, e1 ? atol(e1) : 4L);
+  size_t floor_el = std::max(q, floor_to((e2 ? (size_t)atol(e2) * 1024 : (size_t)32768) / es, q));
+  if (op == OP_REDUCE_SCATTER || op == OP_ALL_GATHER || op == OP_ALL_TO_ALL)
+    floor_el = std::max(q, floor_to(floor_el / (size_t)t.n, q));
+  size_t per_ch = ceil_div(count, (size_t)nch_max * min_tiles);
+  if (per_ch < tile) tile = std::min(tile, std::max(floor_el, ceil_div(per_ch, q) * q));
+  per_ch = ceil_div(count, (size_t)nch_max);
   if (per_ch < tile) tile = std::max(q, ceil_div(per_ch, q) * q);
   g.tile = tile;
   g.ntiles = ceil_div(count, tile);

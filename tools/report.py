@@ -4,7 +4,7 @@
 
 * ar_sweep    : bf16 AR 1 MiB .. 1 GiB (C2), hetccl vs flat NCCL on the same buffers, at the split of N
 * splits      : bf16 AR 256 MiB at every split of N GPUs (1+1; 2+2, 1+3, 1+1+2, 4, singletons)
-* collectives : bf16 RS / AG / Broadcast at 256 MiB (C3 analogue), hetccl vs NCCL
+* collectives : bf16 RS / AG / Broadcast / Reduce / All-to-All at 256 MiB (C3 analogue), hetccl vs NCCL
 * c4          : 1.3e9-element gradients in 25 MiB buckets, issued round-robin on 1/2/4 streams (one comm per
                 stream), wall time per step vs NCCL
 * c5          : Llama-7B gradients (6,738,415,616 elements, 13.5 GB bf16 per rank) in 256 MiB buckets
@@ -197,7 +197,22 @@ def main():
             emit({"row": "broadcast", "split": name, "n": world, "bytes": S, "ms": round(t * 1e3, 4),
                   "busbw": round(S / t / 1e9, 2), "nccl_busbw": round(S / tn / 1e9, 2), "vs_nccl": round(tn / t, 4),
                   "equals_nccl_bitwise": ok})
-            del x, y, ya, yb, yn, zb
+            # reduce (root = last rank) and all-to-all (NEXT-2)
+            yr = torch.empty_like(x) if rank == root else None
+            t = timed(lambda: hc.reduce(x, yr, root, c), args.iters)
+            zr = x.clone()
+            tn = timed(lambda: dist.reduce(zr, dst=root), args.iters)
+            emit({"row": "reduce", "split": name, "n": world, "bytes": S, "ms": round(t * 1e3, 4),
+                  "busbw": round(S / t / 1e9, 2), "nccl_busbw": round(S / tn / 1e9, 2), "vs_nccl": round(tn / t, 4)})
+            y2 = torch.empty_like(x)
+            t = timed(lambda: hc.all_to_all(x, y2, c), args.iters)
+            z2 = torch.empty_like(x)
+            tn = timed(lambda: dist.all_to_all_single(z2, x), args.iters)
+            ok = bool(torch.equal(y2.view(torch.int16), z2.view(torch.int16)))
+            emit({"row": "all_to_all", "split": name, "n": world, "bytes": S, "ms": round(t * 1e3, 4),
+                  "busbw": round(S / t / 1e9 * f, 2), "nccl_busbw": round(S / tn / 1e9 * f, 2),
+                  "vs_nccl": round(tn / t, 4), "equals_nccl_bitwise": ok})
+            del x, y, ya, yb, yn, zb, yr, zr, y2, z2
     elif args.what == "c4":
         name = {2: "1+1", 4: "1+1+2", 8: "2+2+4"}[world]
         m = SPLITS[world][name]
