@@ -134,3 +134,39 @@ def test_trace_stamps_monotone(monkeypatch):
             assert np.all(tr[..., k + 1][used] >= tr[..., k][used])
     finally:
         hc.hetccl_comm_destroy(comm)
+
+
+def test_cuda_graph_replay(monkeypatch):
+    """The protocol keeps its cumulative targets on the device, so a captured All-Reduce (pipeline and
+    one-shot) replays correctly many times; inputs change between replays."""
+    import torch
+    monkeypatch.setenv("HETCCL_ONESHOT_KB", "1024")
+    hc = _hc()
+    m = MAPS["2+2+4"]
+    n = len(m)
+    comm = hc.hetccl_comm_init_mux(n, m, 0)
+    try:
+        for count in (100003, 3 * (1 << 20) + 5):  # one-shot (default cutoff), then pipeline
+            xs0 = inputs("normal", 200, n, count, "bf16")
+            sends = [to_torch(x, "bf16", "cuda") for x in xs0]
+            recvs = [torch.empty_like(s) for s in sends]
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
+                hc.mux_allreduce(sends, recvs, comm, stream=s)  # warm-up outside the graph
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                hc.mux_allreduce(sends, recvs, comm, stream=s)
+            for it in range(12):
+                xs = inputs("normal", 300 + it, n, count, "bf16")
+                for r in range(n):
+                    sends[r].copy_(to_torch(xs[r], "bf16", "cuda"))
+                g.replay()
+                torch.cuda.synchronize()
+                want = oracle.allreduce(xs, m, "bf16", "sum")
+                for r in range(n):
+                    assert np.array_equal(to_numpy(recvs[r], "bf16"), want), f"replay {it} count {count} rank {r}"
+        hc.hetccl_comm_get_async_error(comm)
+    finally:
+        hc.hetccl_comm_destroy(comm)
