@@ -801,14 +801,40 @@ struct ArOp {
           if (q == k) continue;
           const int o = owner_of(tp, q, sg);
           const int dq = tp.dom_size[q];
-          dst.add(slot_ptr<T>(a, o, ch, slot) + s2_off(dq) + (size_t)D * (TL / dq) + (c0 - region_lo(g, o)));
+          if (a.direct) dst.add((T*)a.peer_recv[o] + tb + c0);  // straight into the owner's recv buffer
+          else dst.add(slot_ptr<T>(a, o, ch, slot) + s2_off(dq) + (size_t)D * (TL / dq) + (c0 - region_lo(g, o)));
         }
         for (int i = 0; i < d; i++)
-          if (i != j)
-            dst.add(slot_ptr<T>(a, peer(i), ch, slot) + s2_off(d) + (size_t)(D + 1) * Rk + (size_t)cidx(j, i) * Rk +
-                    (c0 - r0));
+          if (i != j) {
+            if (a.direct) dst.add((T*)a.peer_recv[peer(i)] + tb + c0);
+            else
+              dst.add(slot_ptr<T>(a, peer(i), ch, slot) + s2_off(d) + (size_t)(D + 1) * Rk + (size_t)cidx(j, i) * Rk +
+                      (c0 - r0));
+          }
         cta_fold_hier<T, OP>(inner, k, outer, dst, c1 - c0);
       }
+    } else if (s == 3 && a.direct) {  // ---- D (direct): forward the other owners' pieces (now in y) to peers ----
+      PtrList peers_y;
+      for (int i = 0; i < d; i++)
+        if (i != j) peers_y.add((T*)a.peer_recv[peer(i)] + tb);
+      if (!peers_y.n) return;
+      if (D == 1) {
+        PtrList dst;
+        for (int i = 0; i < peers_y.n; i++) dst.add((const char*)peers_y.p[i] + r0 * ES);
+        cta_copy<ES>(y + tb + r0, dst, r1 - r0);
+      } else {
+        for (int sg = s_lo; sg < s_hi; sg++)
+          for (int q = 0; q < D; q++) {
+            if (q == k) continue;
+            const size_t c0 = g.piece(sg, q), c1 = g.piece(sg, q + 1);
+            if (c1 <= c0) continue;
+            PtrList dst;
+            for (int i = 0; i < peers_y.n; i++) dst.add((const char*)peers_y.p[i] + c0 * ES);
+            cta_copy<ES>(y + tb + c0, dst, c1 - c0);
+          }
+      }
+    } else if (s == 4 && a.direct) {  // ---- E (direct): nothing to copy; the S3 wait made y complete ----
+      return;
     } else if (s == 3) {  // ---- D: the other owners' final pieces of my region -> y and domain peers ----
       PtrList peers_s3;
       for (int i = 0; i < d; i++)

@@ -40,6 +40,7 @@ struct hetcclComm {
   long long timeout_ns = 30LL * 1000000000LL;
   int trace_iters = 0;                    // HETCCL_TRACE_ITERS: per-iteration timestamps of the last op
   int ws = 0;                             // HETCCL_WS: 0 plain pipeline, k in 2..4 warp-specialised (spacing k)
+  int direct = 1;                         // HETCCL_DIRECT: write All-Reduce results straight into peers' recv
   int nslots = 8;                         // HETCCL_NSLOTS: scratch ring depth
   size_t os_bytes = 0;                    // HETCCL_ONESHOT_KB: one-shot AR up to this many bytes per rank
   size_t os_stride = 0;                   // bytes per (buffer, sender) of the one-shot area
@@ -105,6 +106,7 @@ void read_env(hetcclComm* c) {
   c->timeout_ns = (long long)std::max(1L, env_long("HETCCL_TIMEOUT_S", 30)) * 1000000000LL;
   c->trace_iters = (int)std::max(0L, std::min(4096L, env_long("HETCCL_TRACE_ITERS", 0)));
   c->ws = (int)env_long("HETCCL_WS", 0);
+  c->direct = env_long("HETCCL_DIRECT", 1) != 0;
   if (c->ws == 1 || c->ws < 0) c->ws = 0;
   if (c->ws > 4) c->ws = 4;
   c->nslots = (int)std::max(2L, std::min((long)kMaxSlots, env_long("HETCCL_NSLOTS", 8)));
@@ -245,6 +247,11 @@ hetcclResult_t run_op(hetcclComm_t c, int op, const void* const* sends, void* co
   a.timeout_ns = c->timeout_ns;
   a.ws = c->ws;
   a.nslots = c->nslots;
+  // direct recv mode: in a rank-multiplexed comm every rank's recv buffer is a local pointer
+  if (op == OP_ALLREDUCE && c->kind == KIND_MUX && c->direct) {
+    a.direct = 1;
+    for (int r = 0; r < c->n; r++) a.peer_recv[r] = recvs[r];
+  }
   {  // the ring must be deeper than the pipeline (plus the one-iteration release lag of the WS mode)
     int na = 0;
     for (int s = 0; s < kMaxStages; s++) na += (a.active >> s) & 1;
