@@ -209,6 +209,21 @@ HETCCL_API hetcclResult_t hetccl_plan_stages(int nranks, const int* rank_to_doma
                                              hetcclStagePlan_t* plan);
 
 /*
+ * Symmetric recv buffers (SURVEY NEXT-4 "user-buffer registration for zero-copy"). Every rank allocates
+ * a buffer of the same size with hetccl_mem_alloc (device memory of the comm's device, owned by the
+ * comm until hetccl_mem_free / hetccl_comm_destroy), exports it (HETCCL_BLOB_BYTES per rank), the caller
+ * all-gathers the blobs and passes them, concatenated in rank order, to hetccl_mem_connect. From then
+ * on an All-Reduce whose recvbuf lies inside such a buffer is taken to use the SAME offset in every
+ * rank's buffer (the caller's contract), and final results are written straight into the peers'
+ * buffers instead of being staged through scratch. Rank-multiplexed comms need no registration.
+ * HETCCL_DIRECT=0 disables the direct path.
+ */
+HETCCL_API hetcclResult_t hetccl_mem_alloc(hetcclComm_t comm, size_t bytes, void** ptr);
+HETCCL_API hetcclResult_t hetccl_mem_export(hetcclComm_t comm, void* ptr, void* blob, size_t* blob_bytes);
+HETCCL_API hetcclResult_t hetccl_mem_connect(hetcclComm_t comm, void* ptr, const void* blobs, size_t blob_bytes);
+HETCCL_API hetcclResult_t hetccl_mem_free(hetcclComm_t comm, void* ptr);
+
+/*
  * Profiling aid. With HETCCL_TRACE_ITERS=K set when the comm is created, every op records, per
  * (local rank, channel) CTA and pipeline iteration it < K, four globaltimer stamps in ns: wait start,
  * work start (all waits satisfied), work end, release fence done. This copies the LAST op's stamps to

@@ -49,7 +49,7 @@ EXPORTED = [
     "hetccl_reduce_scatter", "hetccl_all_gather", "hetccl_broadcast", "hetccl_mux_allreduce",
     "hetccl_mux_reduce_scatter", "hetccl_mux_all_gather", "hetccl_mux_broadcast", "hetccl_plan_info",
     "hetccl_plan_stages", "hetccl_comm_get_trace", "hetccl_reduce", "hetccl_all_to_all", "hetccl_mux_reduce",
-    "hetccl_mux_all_to_all",
+    "hetccl_mux_all_to_all", "hetccl_mem_alloc", "hetccl_mem_export", "hetccl_mem_connect", "hetccl_mem_free",
 ]
 
 _lib = None
@@ -91,6 +91,10 @@ def lib():
         "hetccl_plan_info": [c_int, ip, c_int, c_int, c_size, c_int, c_int, c_int, ctypes.POINTER(PlanInfo)],
         "hetccl_plan_stages": [c_int, ip, c_int, c_int, c_int, ctypes.POINTER(StagePlan)],
         "hetccl_comm_get_trace": [vp, vp, c_size, ip],
+        "hetccl_mem_alloc": [vp, c_size, pp],
+        "hetccl_mem_export": [vp, vp, vp, ctypes.POINTER(c_size)],
+        "hetccl_mem_connect": [vp, vp, vp, c_size],
+        "hetccl_mem_free": [vp, vp],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -239,6 +243,67 @@ def init_process_group_comm(rank_to_domain, rank=None, world_size=None, device=N
     dist.all_gather_object(blobs, blob, group=group)
     hetccl_comm_connect(comm, blobs)
     return comm
+
+
+# ------------------------------------------------------------------------------ symmetric buffers
+class _CudaArray:
+    """__cuda_array_interface__ view of library-owned device memory (no copy)."""
+
+    def __init__(self, ptr, shape, typestr):
+        self.__cuda_array_interface__ = {"data": (ptr, False), "shape": tuple(shape), "typestr": typestr,
+                                         "version": 3, "strides": None}
+
+
+_TYPESTR = {"float32": "<f4", "float16": "<f2", "int32": "<i4", "bfloat16": "<f2"}
+
+
+def symmetric_empty(comm, numel, dtype, group=None):
+    """Allocate `numel` elements of `dtype` as a symmetric buffer on every rank (collective over `group`,
+    a gloo group works) and connect the peers' copies. Returns a torch tensor viewing the buffer; All-
+    Reduces whose output lies inside it at the same offset on every rank write results straight into the
+    peers' buffers. Free with hetccl_mem_free(comm, t.data_ptr()) or by destroying the comm."""
+    import torch
+    import torch.distributed as dist
+    es = torch.empty((), dtype=dtype).element_size()
+    p = ctypes.c_void_p()
+    _check(lib().hetccl_mem_alloc(comm, numel * es, ctypes.byref(p)), comm)
+    buf = ctypes.create_string_buffer(BLOB_BYTES)
+    nb = ctypes.c_size_t(BLOB_BYTES)
+    _check(lib().hetccl_mem_export(comm, p, buf, ctypes.byref(nb)), comm)
+    blobs = [None] * dist.get_world_size(group)
+    dist.all_gather_object(blobs, buf.raw[: nb.value], group=group)
+    data = b"".join(blobs)
+    _check(lib().hetccl_mem_connect(comm, p, data, len(data)), comm)
+    name = str(dtype).replace("torch.", "")
+    t = torch.as_tensor(_CudaArray(p.value, (numel,), _TYPESTR[name] if name != "bfloat16" else "<i2"),
+                        device="cuda")
+    if dtype == torch.bfloat16:
+        t = t.view(torch.bfloat16)
+    return t
+
+
+def symmetric_empty_all(comms, numel, dtype):
+    """hetccl_comm_init_all comms (one process, n GPUs): a symmetric buffer per device, connected."""
+    import torch
+    es = torch.empty((), dtype=dtype).element_size()
+    ptrs, blobs = [], []
+    for c in comms:
+        p = ctypes.c_void_p()
+        _check(lib().hetccl_mem_alloc(c, numel * es, ctypes.byref(p)), c)
+        buf = ctypes.create_string_buffer(BLOB_BYTES)
+        nb = ctypes.c_size_t(BLOB_BYTES)
+        _check(lib().hetccl_mem_export(c, p, buf, ctypes.byref(nb)), c)
+        ptrs.append(p)
+        blobs.append(buf.raw[: nb.value])
+    data = b"".join(blobs)
+    out = []
+    for i, (c, p) in enumerate(zip(comms, ptrs)):
+        _check(lib().hetccl_mem_connect(c, p, data, len(data)), c)
+        name = str(dtype).replace("torch.", "")
+        t = torch.as_tensor(_CudaArray(p.value, (numel,), _TYPESTR[name] if name != "bfloat16" else "<i2"),
+                            device=f"cuda:{i}")
+        out.append(t.view(torch.bfloat16) if dtype == torch.bfloat16 else t)
+    return out
 
 
 # ------------------------------------------------------------------------------ collectives

@@ -10,6 +10,8 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <unistd.h>
+#include <vector>
 
 #include "../../include/hetccl.h"
 #include "hetccl_internal.h"
@@ -47,6 +49,16 @@ struct hetcclComm {
   unsigned long long* trace = nullptr;
   size_t trace_bytes = 0;
   int trace_shape[2] = {0, 0};            // local ranks, channels of the last traced op
+  // symmetric buffers (hetccl_mem_*): same size on every rank, peers' copies mapped here
+  struct SymBuf {
+    char* base = nullptr;
+    size_t bytes = 0;
+    bool owned = false;                   // allocated by hetccl_mem_alloc
+    bool connected = false;
+    char* peer[kMaxRanks] = {nullptr};
+    bool ipc[kMaxRanks] = {false};
+  };
+  std::vector<SymBuf> sym;
   std::string last_error;
 };
 
@@ -247,10 +259,20 @@ hetcclResult_t run_op(hetcclComm_t c, int op, const void* const* sends, void* co
   a.timeout_ns = c->timeout_ns;
   a.ws = c->ws;
   a.nslots = c->nslots;
-  // direct recv mode: in a rank-multiplexed comm every rank's recv buffer is a local pointer
+  // direct recv mode: in a rank-multiplexed comm every rank's recv buffer is a local pointer; with one
+  // rank per GPU, when recvbuf lies in a connected symmetric buffer (hetccl_mem_*), at the same offset in
+  // every peer's copy
   if (op == OP_ALLREDUCE && c->kind == KIND_MUX && c->direct) {
     a.direct = 1;
     for (int r = 0; r < c->n; r++) a.peer_recv[r] = recvs[r];
+  } else if (op == OP_ALLREDUCE && c->direct) {
+    const char* y = (const char*)recvs[0];
+    for (auto& b : c->sym)
+      if (b.connected && y >= b.base && y + count * (size_t)es <= b.base + b.bytes) {
+        a.direct = 1;
+        for (int r = 0; r < c->n; r++) a.peer_recv[r] = (r == c->rank ? b.base : b.peer[r]) + (y - b.base);
+        break;
+      }
   }
   {  // the ring must be deeper than the pipeline (plus the one-iteration release lag of the WS mode)
     int na = 0;
@@ -480,6 +502,11 @@ hetcclResult_t hetccl_comm_destroy(hetcclComm_t c) {
     }
     if (c->err) cudaFree(c->err);
     if (c->trace) cudaFree(c->trace);
+    for (auto& b : c->sym) {
+      for (int r = 0; r < kMaxRanks; r++)
+        if (b.ipc[r]) cudaIpcCloseMemHandle(b.peer[r]);
+      if (b.owned) cudaFree(b.base);
+    }
   }
   delete c;
   return hetcclSuccess;
@@ -647,6 +674,105 @@ hetcclResult_t hetccl_comm_get_trace(hetcclComm_t c, void* host, size_t bytes, i
   CUDA_TRY(c, cudaDeviceSynchronize());
   CUDA_TRY(c, cudaMemcpy(host, c->trace, need, cudaMemcpyDeviceToHost));
   return hetcclSuccess;
+}
+
+// ------------------------------------------------------------ symmetric buffers (NEXT-4)
+namespace {
+struct MemBlob {
+  uint32_t magic;
+  int rank;
+  int pid;
+  int device;
+  unsigned long long bytes;
+  unsigned long long raw;  // the pointer in the exporting process (used as is within one process)
+  cudaIpcMemHandle_t handle;
+};
+static_assert(sizeof(MemBlob) <= HETCCL_BLOB_BYTES, "mem blob too large");
+constexpr uint32_t kMemMagic = 0x48434d31u;  // "HCM1"
+
+hetcclComm::SymBuf* find_sym(hetcclComm* c, const void* p) {
+  for (auto& b : c->sym)
+    if (b.base == (const char*)p) return &b;
+  return nullptr;
+}
+}  // namespace
+
+hetcclResult_t hetccl_mem_alloc(hetcclComm_t c, size_t bytes, void** ptr) {
+  if (!c || !ptr || bytes == 0) return hetcclInvalidArgument;
+  if (c->kind == KIND_MUX) return fail(c, hetcclInvalidUsage, "symmetric buffers are for one-rank-per-GPU comms");
+  DevGuard g(c->device);
+  hetcclComm::SymBuf b;
+  CUDA_TRY(c, cudaMalloc((void**)&b.base, bytes));
+  b.bytes = bytes;
+  b.owned = true;
+  c->sym.push_back(b);
+  *ptr = b.base;
+  return hetcclSuccess;
+}
+
+hetcclResult_t hetccl_mem_export(hetcclComm_t c, void* ptr, void* blob, size_t* blob_bytes) {
+  if (!c || !ptr || !blob || !blob_bytes) return hetcclInvalidArgument;
+  if (*blob_bytes < HETCCL_BLOB_BYTES) return fail(c, hetcclInvalidArgument, "blob buffer < HETCCL_BLOB_BYTES");
+  hetcclComm::SymBuf* b = find_sym(c, ptr);
+  if (!b) return fail(c, hetcclInvalidArgument, "not a buffer from hetccl_mem_alloc");
+  MemBlob m;
+  memset(&m, 0, sizeof(m));
+  m.magic = kMemMagic;
+  m.rank = c->rank;
+  m.pid = (int)getpid();
+  m.device = c->device;
+  m.bytes = b->bytes;
+  m.raw = (unsigned long long)(uintptr_t)b->base;
+  DevGuard g(c->device);
+  CUDA_TRY(c, cudaIpcGetMemHandle(&m.handle, b->base));
+  memset(blob, 0, HETCCL_BLOB_BYTES);
+  memcpy(blob, &m, sizeof(m));
+  *blob_bytes = HETCCL_BLOB_BYTES;
+  return hetcclSuccess;
+}
+
+hetcclResult_t hetccl_mem_connect(hetcclComm_t c, void* ptr, const void* blobs, size_t blob_bytes) {
+  if (!c || !ptr || !blobs) return hetcclInvalidArgument;
+  if (!c->connected) return fail(c, hetcclInvalidUsage, "comm is not connected");
+  if (blob_bytes != (size_t)c->n * HETCCL_BLOB_BYTES)
+    return fail(c, hetcclInvalidArgument, "expected %d blobs of %d bytes", c->n, HETCCL_BLOB_BYTES);
+  hetcclComm::SymBuf* b = find_sym(c, ptr);
+  if (!b) return fail(c, hetcclInvalidArgument, "not a buffer from hetccl_mem_alloc");
+  DevGuard g(c->device);
+  for (int r = 0; r < c->n; r++) {
+    MemBlob m;
+    memcpy(&m, (const char*)blobs + (size_t)r * HETCCL_BLOB_BYTES, sizeof(m));
+    if (m.magic != kMemMagic || m.rank != r) return fail(c, hetcclInvalidUsage, "blob %d is not a hetccl mem blob", r);
+    if (m.bytes != b->bytes) return fail(c, hetcclInvalidUsage, "rank %d registered %llu bytes, not %zu", r, m.bytes, b->bytes);
+    if (r == c->rank) continue;
+    if (m.pid == (int)getpid()) {  // same process (hetccl_comm_init_all): peer access is enabled
+      b->peer[r] = (char*)(uintptr_t)m.raw;
+    } else {
+      void* p = nullptr;
+      cudaError_t e = cudaIpcOpenMemHandle(&p, m.handle, cudaIpcMemLazyEnablePeerAccess);
+      if (e != cudaSuccess) return fail(c, hetcclSystemError, "cudaIpcOpenMemHandle(rank %d): %s", r, cudaGetErrorString(e));
+      b->peer[r] = (char*)p;
+      b->ipc[r] = true;
+    }
+  }
+  b->connected = true;
+  return hetcclSuccess;
+}
+
+hetcclResult_t hetccl_mem_free(hetcclComm_t c, void* ptr) {
+  if (!c || !ptr) return hetcclInvalidArgument;
+  for (size_t i = 0; i < c->sym.size(); i++) {
+    auto& b = c->sym[i];
+    if (b.base != (char*)ptr) continue;
+    DevGuard g(c->device);
+    cudaDeviceSynchronize();
+    for (int r = 0; r < kMaxRanks; r++)
+      if (b.ipc[r]) cudaIpcCloseMemHandle(b.peer[r]);
+    if (b.owned) cudaFree(b.base);
+    c->sym.erase(c->sym.begin() + i);
+    return hetcclSuccess;
+  }
+  return fail(c, hetcclInvalidArgument, "not a buffer from hetccl_mem_alloc");
 }
 
 }  // extern "C"

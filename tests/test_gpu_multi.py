@@ -92,3 +92,46 @@ def test_c1_fp32_1mi_bitexact():
         finally:
             for c in comms:
                 hc.hetccl_comm_destroy(c)
+
+
+@pytest.mark.parametrize("name", ["1+1", "2+2", "1+3", "1+1+2", "4"])
+@pytest.mark.parametrize("inplace", [False, True])
+def test_allreduce_symmetric_direct(name, inplace, monkeypatch):
+    """Symmetric recv buffers (hetccl_mem_*): final pieces are written straight into the peers' buffers;
+    results bitwise equal to the oracle, at an offset inside the buffer, in and out of place."""
+    import torch
+    import paper_2601_22585_b200 as hc
+    m = MAPS[name]
+    n = len(m)
+    if _ngpu() < n:
+        pytest.skip(f"needs {n} GPUs")
+    monkeypatch.setenv("HETCCL_TILE_KB", "16")
+    monkeypatch.setenv("HETCCL_ONESHOT_KB", "0")
+    count, off = 5 * 8192 + 333, 1000
+    xs = inputs("normal", 17, n, count, "bf16")
+    comms = _comms(m)
+    try:
+        bufs = hc.symmetric_empty_all(comms, count + 2 * off, torch.bfloat16)
+        for it in range(3):
+            xs = inputs("normal", 17 + it, n, count, "bf16")
+            sends = []
+            for r in range(n):
+                bufs[r].fill_(0)
+                if inplace:
+                    bufs[r][off:off + count].copy_(to_torch(xs[r], "bf16", f"cuda:{r}"))
+                    sends.append(bufs[r][off:off + count])
+                else:
+                    sends.append(to_torch(xs[r], "bf16", f"cuda:{r}"))
+            _sync(n)
+            for r in range(n):
+                with torch.cuda.device(r):
+                    hc.allreduce(sends[r], bufs[r][off:off + count], comms[r])
+            _sync(n)
+            want = oracle.allreduce(xs, m, "bf16", "sum")
+            for r in range(n):
+                hc.hetccl_comm_get_async_error(comms[r])
+                assert np.array_equal(to_numpy(bufs[r][off:off + count], "bf16"), want), f"{name} it {it} rank {r}"
+                assert not to_numpy(bufs[r][:off], "bf16").any(), "wrote outside the recv range"
+    finally:
+        for c in comms:
+            hc.hetccl_comm_destroy(c)
