@@ -45,6 +45,36 @@ def build(force=False, verbose=False, variant=None, defines=()):
     return lib
 
 
+NCCL_INC = os.path.join(os.path.dirname(os.path.dirname(os.__file__)), "site-packages", "nvidia", "nccl", "include")
+SHIM = os.path.join(HERE, "libhetccl_nccl.so")
+
+
+def nccl_include():
+    try:
+        import nvidia.nccl as nn
+        return os.path.join(list(nn.__path__)[0], "include")
+    except Exception:
+        return NCCL_INC
+
+
+def build_shim(force=False):
+    """libhetccl_nccl.so: LD_PRELOAD interposition of NCCL's collectives onto libhetccl.so (NEXT-4)."""
+    src = os.path.join(CSRC, "nccl_shim.cpp")
+    if not force and os.path.exists(SHIM) and os.path.getmtime(SHIM) > max(os.path.getmtime(src), os.path.getmtime(LIB)):
+        return SHIM
+    tmp = SHIM + f".tmp{os.getpid()}"
+    cmd = [NVCC, "-O2", "-std=c++17", "-x", "cu", "-gencode", "arch=compute_100a,code=sm_100a", "-Xcompiler",
+           "-fPIC,-fvisibility=hidden", "--shared", "-cudart", "static", f"-I{nccl_include()}", src, "-o", tmp,
+           f"-L{HERE}", "-lhetccl", "-Xlinker", "-rpath,$ORIGIN", "-ldl"]
+    p = subprocess.run(cmd, capture_output=True, text=True)
+    if p.returncode != 0:
+        sys.stderr.write(p.stdout + p.stderr)
+        raise RuntimeError("nvcc failed building libhetccl_nccl.so")
+    os.replace(tmp, SHIM)
+    return SHIM
+
+
 if __name__ == "__main__":
     build(force="--force" in sys.argv, verbose=True)
-    print(LIB)
+    build_shim(force="--force" in sys.argv)
+    print(LIB, SHIM)
