@@ -130,8 +130,14 @@ def main():
         graph = mib <= 16  # launch-latency regime: time CUDA-graph replays (both libraries)
         if graph:
             it = 50
-        t = timed(lambda: hc.allreduce(x, y, c), it, graph=graph)
+        t_staged = timed(lambda: hc.allreduce(x, y, c), it, graph=graph)
         ok = parity_ar(y, seed, count, m)
+        # symmetric recv buffer (hetccl_mem_*): results written straight into the peers' buffers
+        ysym = hc.symmetric_empty(c, count, torch.bfloat16, group=gloo)
+        t = timed(lambda: hc.allreduce(x, ysym, c), it, graph=graph)
+        ok = ok and parity_ar(ysym, seed, count, m)
+        hc.lib().hetccl_mem_free(c, ysym.data_ptr())
+        del ysym
         z = x.clone()
         tn = timed(lambda: dist.all_reduce(z), it, graph=graph)
         alg = S / t / 1e9
@@ -141,7 +147,9 @@ def main():
         emit({"row": "allreduce", "split": name, "map": m, "n": world, "bytes": S, "dtype": "bf16", "ms": round(t * 1e3, 4),
               "algbw": round(alg, 2), "busbw": round(bus, 2), "nccl_busbw": round(nbus, 2),
               "vs_nccl": round(bus / nbus, 4), "busbw_over_900": round(bus / 900, 4),
-              "link_util_770": round(busiest / t / 1e9 / 770, 4), "r7_gate": ok, "cuda_graph": graph})
+              "link_util_770": round(busiest / t / 1e9 / 770, 4), "r7_gate": ok, "cuda_graph": graph,
+              "staged_busbw": round(S / t_staged / 1e9 * 2 * (world - 1) / world, 2),
+              "note": "busbw: recv in a symmetric buffer (direct); staged_busbw: plain torch recv buffer"})
         del x, y, z
 
     if args.what == "ar_sweep":
