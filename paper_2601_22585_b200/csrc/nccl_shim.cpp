@@ -34,10 +34,26 @@ std::mutex g_mu;
 std::unordered_map<ncclComm_t, hetcclComm_t> g_map;
 std::atomic<long> g_routed{0}, g_passed{0};
 
+// The real NCCL: RTLD_NEXT finds it when libnccl is in the global scope; Python extension modules load
+// it RTLD_LOCAL (torch), so fall back to the already-loaded libnccl.so.2 (RTLD_NOLOAD), else HETCCL_NCCL_LIB.
+void* nccl_handle() {
+  static void* h = [] {
+    void* x = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!x) {
+      const char* e = getenv("HETCCL_NCCL_LIB");
+      x = dlopen(e && *e ? e : "libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+    }
+    return x;
+  }();
+  return h;
+}
+
 template <typename F>
 F real(const char* name) {
   static_assert(sizeof(F) == sizeof(void*), "fn ptr");
-  void* p = dlsym(RTLD_NEXT, name);
+  void* p = nullptr;
+  if (void* h = nccl_handle()) p = dlsym(h, name);
+  if (!p) p = dlsym(RTLD_NEXT, name);
   if (!p) {
     fprintf(stderr, "hetccl shim: cannot resolve %s\n", name);
     abort();
