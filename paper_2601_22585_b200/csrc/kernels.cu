@@ -1243,32 +1243,32 @@ struct A2aOp {
 
 // ================================================================== kernels ===================
 template <typename T, int OP>
-__global__ void __launch_bounds__(kThreads, 1) k_allreduce(const __grid_constant__ OpArgs a) {
+__global__ void __launch_bounds__(kThreads, kCtasPerSm) k_allreduce(const __grid_constant__ OpArgs a) {
   ArOp<T, OP> op(a, blockIdx.y, blockIdx.x);
   run_pipeline(a, op, op.me, blockIdx.x);
 }
 template <typename T, int OP>
-__global__ void __launch_bounds__(kThreads, 1) k_reduce_scatter(const __grid_constant__ OpArgs a) {
+__global__ void __launch_bounds__(kThreads, kCtasPerSm) k_reduce_scatter(const __grid_constant__ OpArgs a) {
   RsOp<T, OP> op(a, blockIdx.y, blockIdx.x);
   run_pipeline(a, op, op.me, blockIdx.x);
 }
 template <typename T>
-__global__ void __launch_bounds__(kThreads, 1) k_all_gather(const __grid_constant__ OpArgs a) {
+__global__ void __launch_bounds__(kThreads, kCtasPerSm) k_all_gather(const __grid_constant__ OpArgs a) {
   AgOp<T> op(a, blockIdx.y, blockIdx.x);
   run_pipeline(a, op, op.me, blockIdx.x);
 }
 template <typename T, int OP>
-__global__ void __launch_bounds__(kThreads, 1) k_reduce(const __grid_constant__ OpArgs a) {
+__global__ void __launch_bounds__(kThreads, kCtasPerSm) k_reduce(const __grid_constant__ OpArgs a) {
   RdOp<T, OP> op(a, blockIdx.y, blockIdx.x);
   run_pipeline(a, op, op.me, blockIdx.x);
 }
 template <typename T>
-__global__ void __launch_bounds__(kThreads, 1) k_all_to_all(const __grid_constant__ OpArgs a) {
+__global__ void __launch_bounds__(kThreads, kCtasPerSm) k_all_to_all(const __grid_constant__ OpArgs a) {
   A2aOp<T> op(a, blockIdx.y, blockIdx.x);
   run_pipeline(a, op, op.me, blockIdx.x);
 }
 template <typename T>
-__global__ void __launch_bounds__(kThreads, 1) k_broadcast(const __grid_constant__ OpArgs a) {
+__global__ void __launch_bounds__(kThreads, kCtasPerSm) k_broadcast(const __grid_constant__ OpArgs a) {
   BcOp<T> op(a, blockIdx.y, blockIdx.x);
   run_pipeline(a, op, op.me, blockIdx.x);
 }
@@ -1280,7 +1280,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_broadcast(const __grid_constant
 // order (cta_fold_domains) — bitwise identical to the hierarchical path, one round trip.
 // Counters per (channel, sender): C_OS (data of op g landed), C_OSACK (op g's buffer consumed).
 template <typename T, int OP>
-__global__ void __launch_bounds__(kThreads, 1) k_allreduce_oneshot(const __grid_constant__ OpArgs a) {
+__global__ void __launch_bounds__(kThreads, kCtasPerSm) k_allreduce_oneshot(const __grid_constant__ OpArgs a) {
   constexpr int V = Tr<T>::V;
   const int row = blockIdx.y, ch = blockIdx.x;
   const int me = a.local_rank[row], n = a.topo.n;

@@ -31,7 +31,7 @@ struct hetcclComm {
   int n = 0, rank = 0, device = 0;
   int map[kMaxRanks] = {0};
   Topo topo{};
-  int nch_max = 148;
+  int nch_max = kMaxChannels;
   size_t slot_bytes = 0;
   size_t alloc_bytes = 0;
   char* local[kMaxRanks] = {nullptr};    // allocations owned by this comm (mux: one per rank)
@@ -109,7 +109,7 @@ size_t alloc_bytes_for(const hetcclComm* c) {
 }
 
 void read_env(hetcclComm* c) {
-  c->nch_max = (int)std::max(1L, std::min((long)kMaxChannels, env_long("HETCCL_NCHANNELS", 148)));
+  c->nch_max = (int)std::max(1L, std::min((long)kMaxChannels, env_long("HETCCL_NCHANNELS", kMaxChannels)));
   // scratch slot: HETCCL_SLOT_KB, else sized from this map so every op's default tile fits
   const long slot_kb = env_long("HETCCL_SLOT_KB", 0);
   c->slot_bytes = slot_kb > 0 ? (size_t)std::max(64L, slot_kb) * 1024
@@ -470,7 +470,7 @@ hetcclResult_t hetccl_comm_init_mux(hetcclComm_t* comm, int nranks, const int* r
   {  // all ranks' CTAs must be co-resident (one per SM): channels per rank <= SMs / nranks
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cuda_device);
-    c->nch_max = std::max(1, std::min(c->nch_max, sms / nranks));
+    c->nch_max = std::max(1, std::min(c->nch_max, sms * kCtasPerSm / nranks));
     c->alloc_bytes = alloc_bytes_for(c);
   }
   cudaError_t e = cudaSuccess;
