@@ -225,9 +225,10 @@ HETCCL_API hetcclResult_t hetccl_mem_free(hetcclComm_t comm, void* ptr);
 
 /*
  * Profiling aid. With HETCCL_TRACE_ITERS=K set when the comm is created, every op records, per
- * (local rank, channel) CTA and pipeline iteration it < K, four globaltimer stamps in ns: wait start,
- * work start (all waits satisfied), work end, release fence done. This copies the LAST op's stamps to
- * `host` as uint64 [shape0 local ranks][shape1 channels][shape2 = K iterations][4] (synchronizes
+ * (local rank, channel) CTA and pipeline iteration it < K, eight globaltimer stamps in ns: wait start,
+ * work start (all waits satisfied), work end, release fence done, and the end of logical stages 0..3 as
+ * seen by thread 0 (0 if the stage did not run). This copies the LAST op's stamps to
+ * `host` as uint64 [shape0 local ranks][shape1 channels][shape2 = K iterations][8] (synchronizes
  * the device; unused iterations are 0). shape[0..2] are written; all zero if tracing is off. With
  * host == NULL only the shape is written.
  */

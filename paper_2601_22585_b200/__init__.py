@@ -201,13 +201,14 @@ def hetccl_comm_get_async_error(comm):
 
 def hetccl_comm_get_trace(comm):
     """Per-iteration timestamps of the last op (HETCCL_TRACE_ITERS at comm creation): numpy uint64
-    array [local ranks, channels, iterations, 4] (wait start, work start, work end, fenced), or None."""
+    array [local ranks, channels, iterations, 8] (wait start, work start, work end, fenced, end of logical
+    stages 0..3 on thread 0 — 0 where the stage did not run), or None."""
     import numpy as np
     shape = (ctypes.c_int * 3)()
     _check(lib().hetccl_comm_get_trace(comm, None, 0, shape), comm)
     if shape[0] == 0:
         return None
-    out = np.zeros((shape[0], shape[1], shape[2], 4), np.uint64)
+    out = np.zeros((shape[0], shape[1], shape[2], 8), np.uint64)
     _check(lib().hetccl_comm_get_trace(comm, out.ctypes.data, out.nbytes, shape), comm)
     return out
 

@@ -30,6 +30,7 @@ constexpr int kMaxSlots = 16;      // cap on the scratch ring depth per channel 
 #endif
 constexpr int kThreads = HETCCL_THREADS;  // threads per CTA (one CTA per SM)
 constexpr int kMaxStages = 5;      // pipeline positions of the deepest op (All-Reduce)
+constexpr int kTraceWords = 8;     // per traced iteration: poll start, GO, DONE, fenced, end of stages 0..3
 
 // counters (per rank, per channel); C_ACK counts tiles a sender has fully consumed
 // C_OS / C_OSACK belong to the one-shot small-message All-Reduce (k_allreduce_oneshot).

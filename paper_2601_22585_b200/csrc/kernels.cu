@@ -609,11 +609,14 @@ struct Pipe {
     long long tl;
     if (last >= 0 && tile_at(it, last, tl)) red_add_relaxed_sys(chan_flags(a, lane, ch) + C_ACK * kLineWords + me, 1);
   }
+  unsigned long long* trc = nullptr;  // per-iteration stamps (HETCCL_TRACE_ITERS), thread 0 only
   __device__ void work(long long it) {
     for (int p = 0; p < npos; p++) {
       long long tl;
       if (stage_at[p] < 0 || !tile_at(it, p, tl)) continue;
       op.stage(stage_at[p], (size_t)ch + (size_t)tl * a.nch, (int)((tiles0 + tl) % (unsigned long long)a.nslots));
+      if (trc && threadIdx.x == 0 && it < a.trace_iters && stage_at[p] < 4)
+        trc[it * kTraceWords + 4 + stage_at[p]] = globaltimer();
     }
   }
 };
@@ -649,10 +652,11 @@ __device__ __forceinline__ void run_pipeline(const OpArgs& a, Op& op, int me, in
   P.tiles0 = ps.tiles0;
   const long long nit = P.ntl > 0 ? P.ntl + P.npos - 1 : 0;
   const bool sync_warp = threadIdx.x < 32;
-  unsigned long long* trc = nullptr;  // [it][4] globaltimer stamps: poll start, GO, DONE, fenced
-  if (a.trace) trc = a.trace + ((size_t)blockIdx.y * gridDim.x + ch) * (size_t)a.trace_iters * 4;
+  unsigned long long* trc = nullptr;  // [it][kTraceWords] globaltimer stamps: poll start, GO, DONE, fenced, stage ends
+  if (a.trace) trc = a.trace + ((size_t)blockIdx.y * gridDim.x + ch) * (size_t)a.trace_iters * kTraceWords;
+  P.trc = trc;
   auto stamp = [&](long long it, int k) {
-    if (trc && threadIdx.x == 0 && it >= 0 && it < a.trace_iters) trc[it * 4 + k] = globaltimer();
+    if (trc && threadIdx.x == 0 && it >= 0 && it < a.trace_iters) trc[it * kTraceWords + k] = globaltimer();
   };
   if (ws) {
     if (sync_warp && nit > 0) {

@@ -282,7 +282,7 @@ hetcclResult_t run_op(hetcclComm_t c, int op, const void* const* sends, void* co
       return fail(c, hetcclInvalidUsage, "HETCCL_NSLOTS=%d must exceed the pipeline depth %d", c->nslots, npos);
   }
   if (c->trace_iters > 0) {
-    const size_t need = (size_t)nlocal * geo.nch * c->trace_iters * 4 * sizeof(unsigned long long);
+    const size_t need = (size_t)nlocal * geo.nch * c->trace_iters * kTraceWords * sizeof(unsigned long long);
     if (need > c->trace_bytes) {
       if (c->trace) cudaFree(c->trace);
       c->trace = nullptr;
@@ -663,7 +663,7 @@ hetcclResult_t hetccl_comm_get_trace(hetcclComm_t c, void* host, size_t bytes, i
   shape[0] = c->trace_shape[0];
   shape[1] = c->trace_shape[1];
   shape[2] = c->trace_iters;
-  const size_t need = (size_t)shape[0] * shape[1] * shape[2] * 4 * sizeof(unsigned long long);
+  const size_t need = (size_t)shape[0] * shape[1] * shape[2] * kTraceWords * sizeof(unsigned long long);
   if (!c->trace || need == 0) {
     shape[0] = shape[1] = shape[2] = 0;
     return hetcclSuccess;

@@ -127,7 +127,7 @@ def test_trace_stamps_monotone(monkeypatch):
         ys = [torch.empty_like(x) for x in xs]
         hc.mux_allreduce(xs, ys, comm)
         tr = hc.hetccl_comm_get_trace(comm)
-        assert tr is not None and tr.shape[0] == 4 and tr.shape[3] == 4
+        assert tr is not None and tr.shape[0] == 4 and tr.shape[3] == 8
         used = tr[..., 0] > 0
         assert used.any()
         for k in range(3):

@@ -31,6 +31,18 @@ def summarize(tr, label):
           f"per iteration mean wait {wait.mean() / 1e3:.2f} us, work {work.mean() / 1e3:.2f} us, "
           f"fence {fence.mean() / 1e3:.2f} us; p90 wait {np.percentile(wait, 90) / 1e3:.2f} "
           f"work {np.percentile(work, 90) / 1e3:.2f} fence {np.percentile(fence, 90) / 1e3:.2f}")
+    # per logical stage: time from the previous stamp (work start or the previous stage's end)
+    st = tr[..., 4:8].astype(np.int64)
+    prev = tr[..., 1].astype(np.int64)
+    names = "ABCD"
+    parts = []
+    for s in range(4):
+        m = used & (st[..., s] > 0)
+        if m.any():
+            parts.append(f"{names[s]} {(st[..., s] - prev)[m].mean() / 1e3:.2f}")
+            prev = np.where(st[..., s] > 0, st[..., s], prev)
+    tail = (tr[..., 2].astype(np.int64) - prev)[used]
+    print("  per stage (us, mean over iterations where it ran): " + ", ".join(parts) + f", E/rest {tail.mean() / 1e3:.2f}")
     # by iteration index (mean over channels/rows)
     for it in list(range(min(6, iters))) + [iters // 2]:
         m = used[..., it]
@@ -46,6 +58,7 @@ def main():
     ap.add_argument("--mib", type=int, default=256)
     ap.add_argument("--op", default="ar")
     ap.add_argument("--out", default="gpurun_out/trace")
+    ap.add_argument("--sym", action="store_true", help="All-Reduce into a symmetric buffer (direct path)")
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -75,7 +88,7 @@ def main():
     count = args.mib * (1 << 20) // 2
     x = torch.randn(count, device="cuda").bfloat16()
     if args.op == "ar":
-        y = torch.empty_like(x)
+        y = hc.symmetric_empty(comm, count, torch.bfloat16) if args.sym else torch.empty_like(x)
         fn = lambda: hc.allreduce(x, y, comm)
     elif args.op == "rs":
         y = torch.empty(count // world, dtype=x.dtype, device="cuda")
