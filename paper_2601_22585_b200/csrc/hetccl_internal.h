@@ -20,13 +20,13 @@ namespace hetccl {
 
 constexpr int kMaxRanks = 16;      // == HETCCL_MAX_RANKS (one flag line = 16 senders x 8 B)
 #ifndef HETCCL_CTAS_PER_SM
-#define HETCCL_CTAS_PER_SM 1
+#define HETCCL_CTAS_PER_SM 2
 #endif
 constexpr int kCtasPerSm = HETCCL_CTAS_PER_SM;     // resident CTAs per SM the kernels are built for
 constexpr int kMaxChannels = 148 * kCtasPerSm;     // hard cap on CTAs per rank per op
 constexpr int kMaxSlots = 16;      // cap on the scratch ring depth per channel (HETCCL_NSLOTS)
 #ifndef HETCCL_THREADS
-#define HETCCL_THREADS 256
+#define HETCCL_THREADS 128
 #endif
 constexpr int kThreads = HETCCL_THREADS;  // threads per CTA (one CTA per SM)
 constexpr int kMaxStages = 5;      // pipeline positions of the deepest op (All-Reduce)
