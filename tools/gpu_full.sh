@@ -19,7 +19,7 @@ for n in 2 4; do
     echo "report $w n=$n rc=$?" >> $O/report_rc.txt
   done
   HETCCL_TRACE_ITERS=256 timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 \
-    --master-port 2990$n tools/trace_run.py --out $O/trace_n$n >> $O/trace.txt 2>&1
+    --master-port 2990$n tools/trace_run.py --sym --out $O/trace_n$n >> $O/trace.txt 2>&1
 done
 timeout 300 python bench.py --impl reference > $O/ref1.json 2> $O/ref1.err
 CMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline"

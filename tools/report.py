@@ -228,12 +228,16 @@ def main():
         bucket = 25 * (1 << 20) // 2
         sizes = [bucket] * (total // bucket) + ([total % bucket] if total % bucket else [])
         g = bf16_inputs(4, total)
-        out_g = torch.empty_like(g)
+        # the reduced-gradient buffer is symmetric (hetccl_mem_*), one per stream comm set: results land
+        # straight in the peers' buffers; comms of every stream count connect to the first one's buffer
+        out_g = None
         offs = np.cumsum([0] + sizes)
         for nstreams in (1, 2, 4):
             streams = [torch.cuda.Stream() for _ in range(nstreams)]
             # concurrent persistent kernels must be co-resident: split the SMs between the streams' comms
-            cs = [comm_for(name, m, slot=i, nch=148 // nstreams) for i in range(nstreams)]
+            cs = [comm_for(name, m, slot=i, nch=296 // nstreams) for i in range(nstreams)]
+            outs = [hc.symmetric_empty(c, total, torch.bfloat16, group=gloo) for c in cs]
+            out_g = outs[0]
             cur = torch.cuda.current_stream()
 
             def step():
@@ -241,11 +245,17 @@ def main():
                     s.wait_stream(cur)
                 for b, sz in enumerate(sizes):
                     i = b % nstreams
-                    hc.hetccl_allreduce(g[offs[b]:].data_ptr(), out_g[offs[b]:].data_ptr(), int(sz), hc.BFLOAT16, "sum",
-                                        cs[i], streams[i].cuda_stream)
+                    hc.hetccl_allreduce(g[offs[b]:].data_ptr(), outs[i][offs[b]:].data_ptr(), int(sz), hc.BFLOAT16,
+                                        "sum", cs[i], streams[i].cuda_stream)
                 for s in streams:
                     cur.wait_stream(s)
             t = timed(step, 3, warm=1)
+            if nstreams > 1:  # bucket b was reduced into outs[b % nstreams]; gather the result into out_g
+                for b, sz in enumerate(sizes):
+                    if b % nstreams:
+                        out_g[offs[b]:offs[b] + sz].copy_(outs[b % nstreams][offs[b]:offs[b] + sz])
+            for c, o in zip(cs[1:], outs[1:]):
+                hc.lib().hetccl_mem_free(c, o.data_ptr())
             emit({"row": "c4_buckets", "split": name, "n": world, "streams": nstreams, "buckets": len(sizes),
                   "bytes": total * 2, "ms": round(t * 1e3, 3),
                   "eff_busbw": round(total * 2 / t / 1e9 * 2 * (world - 1) / world, 2)})
@@ -265,9 +275,9 @@ def main():
         total = 6_738_415_616
         bucket = 256 * (1 << 20) // 2
         sizes = [bucket] * (total // bucket) + ([total % bucket] if total % bucket else [])
-        g = torch.empty(total, dtype=torch.bfloat16, device="cuda")
-        g.normal_(0, 1.0 / 16, generator=torch.Generator("cuda").manual_seed(5 + rank))
         c = comm_for(name, m)
+        g = hc.symmetric_empty(c, total, torch.bfloat16, group=gloo)  # the gradient buffer is symmetric
+        g.normal_(0, 1.0 / 16, generator=torch.Generator("cuda").manual_seed(5 + rank))
         offs = np.cumsum([0] + sizes)
 
         def step():
