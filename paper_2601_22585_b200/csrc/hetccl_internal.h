@@ -112,6 +112,8 @@ struct OpArgs {
   int nslots;                   // scratch ring depth (> pipeline positions)
   size_t os_off;                // one-shot area: byte offset in every rank's scratch, bytes per (buffer, sender)
   size_t os_stride;
+  int final_stage;              // logical stage whose waits become ONE end-of-kernel wait (no pipeline
+                                //   position; its work must be empty), or -1
   int direct;                   // 1: every rank's recv buffer is addressable here (peer_recv), so All-Reduce
   void* peer_recv[kMaxRanks];   //    writes final pieces straight into them (no staging through scratch)
 };

@@ -637,7 +637,7 @@ __device__ __forceinline__ void run_pipeline(const OpArgs& a, Op& op, int me, in
   for (int p = 0; p < 4 * kMaxStages; p++) P.stage_at[p] = -1;
 #pragma unroll
   for (int s = 0; s < kMaxStages; s++)
-    if ((a.active >> s) & 1u) P.stage_at[P.SP * P.np++] = s;
+    if (((a.active >> s) & 1u) && s != a.final_stage) P.stage_at[P.SP * P.np++] = s;
   P.npos = P.SP * (P.np - 1) + 1;
   if (threadIdx.x < kCounters * kMaxRanks)
     ps.base[threadIdx.x / kMaxRanks][threadIdx.x % kMaxRanks] = B[threadIdx.x / kMaxRanks * kLineWords + threadIdx.x % kMaxRanks];
@@ -702,6 +702,25 @@ __device__ __forceinline__ void run_pipeline(const OpArgs& a, Op& op, int me, in
         fence_acq_rel_sys();
         stamp(it, 3);
         P.signal(it);
+      }
+    }
+  }
+  // ---- final stage (direct All-Reduce's E): one wait for every tile's signal instead of a position ----
+  if (a.final_stage >= 0 && ((a.active >> a.final_stage) & 1u) && threadIdx.x < 32 && P.lane < P.n &&
+      !*(volatile int*)&ps.abort_) {
+    const RankPlan& rp = a.rp[me];
+    const int wc = rp.wait_ctr[a.final_stage];
+    if (wc != C_NONE && ((rp.wait_mask[a.final_stage] >> P.lane) & 1u)) {
+      const uint64_t* w = P.F + wc * kLineWords + P.lane;
+      const uint64_t tg = ps.base[wc][P.lane] + P.ntl;
+      const uint64_t t0 = globaltimer();
+      uint32_t spins = 0;
+      while (ld_acquire_sys(w) < tg) {
+        if ((++spins & 1023u) == 0 && (long long)(globaltimer() - t0) > a.timeout_ns) {
+          atomicOr(a.err, 1ull + ((unsigned long long)wc << 8) + ((unsigned long long)P.lane << 16));
+          ps.abort_ = 1;
+          break;
+        }
       }
     }
   }

@@ -262,6 +262,7 @@ hetcclResult_t run_op(hetcclComm_t c, int op, const void* const* sends, void* co
   // direct recv mode: in a rank-multiplexed comm every rank's recv buffer is a local pointer; with one
   // rank per GPU, when recvbuf lies in a connected symmetric buffer (hetccl_mem_*), at the same offset in
   // every peer's copy
+  a.final_stage = -1;
   if (op == OP_ALLREDUCE && c->kind == KIND_MUX && c->direct) {
     a.direct = 1;
     for (int r = 0; r < c->n; r++) a.peer_recv[r] = recvs[r];
@@ -274,6 +275,8 @@ hetcclResult_t run_op(hetcclComm_t c, int op, const void* const* sends, void* co
         break;
       }
   }
+  // direct All-Reduce: stage E has no data, only its S3 wait (my y is complete) -> one end-of-kernel wait
+  if (a.direct && env_long("HETCCL_FINAL_WAIT", 1)) a.final_stage = 4;
   {  // the ring must be deeper than the pipeline (plus the one-iteration release lag of the WS mode)
     int na = 0;
     for (int s = 0; s < kMaxStages; s++) na += (a.active >> s) & 1;
