@@ -651,6 +651,31 @@ __device__ __forceinline__ void run_pipeline(const OpArgs& a, Op& op, int me, in
   P.ntl = (ch < (long long)a.ntiles) ? ((long long)a.ntiles - ch + a.nch - 1) / a.nch : 0;
   P.tiles0 = ps.tiles0;
   const long long nit = P.ntl > 0 ? P.ntl + P.npos - 1 : 0;
+  // pull mode: my domain peers read my send buffer directly, so they must not start before it is ready
+  // (this op started here): one release-signal / acquire-wait round per channel on counter S1
+  if (a.pull && P.ntl > 0) {
+    if (threadIdx.x < 32) {
+      const Topo& tp = a.topo;
+      const int k = tp.rank_dom[me];
+      const bool dpeer = P.lane < P.n && P.lane != me && tp.rank_dom[P.lane] == k;
+      fence_acq_rel_sys();
+      if (dpeer) red_add_relaxed_sys(chan_flags(a, P.lane, ch) + C_S1 * kLineWords + me, 1);
+      if (dpeer) {
+        const uint64_t* w = P.F + C_S1 * kLineWords + P.lane;
+        const uint64_t tg = ps.base[C_S1][P.lane] + 1;
+        const uint64_t t0 = globaltimer();
+        uint32_t spins = 0;
+        while (ld_acquire_sys(w) < tg) {
+          if ((++spins & 1023u) == 0 && (long long)(globaltimer() - t0) > a.timeout_ns) {
+            atomicOr(a.err, 1ull + ((unsigned long long)C_S1 << 8) + ((unsigned long long)P.lane << 16));
+            ps.abort_ = 1;
+            break;
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
   const bool sync_warp = threadIdx.x < 32;
   unsigned long long* trc = nullptr;  // [it][kTraceWords] globaltimer stamps: poll start, GO, DONE, fenced, stage ends
   if (a.trace) trc = a.trace + ((size_t)blockIdx.y * gridDim.x + ch) * (size_t)a.trace_iters * kTraceWords;
@@ -735,6 +760,8 @@ __device__ __forceinline__ void run_pipeline(const OpArgs& a, Op& op, int me, in
       if (wc != C_NONE && ((rp.wait_mask[s] >> p) & 1u)) B[wc * kLineWords + p] = ps.base[wc][p] + P.ntl;
     }
     if (p == 0) B[kCounters * kLineWords] = P.tiles0 + P.ntl;
+    if (a.pull && P.ntl > 0 && p < P.n && p != me && a.topo.rank_dom[p] == a.topo.rank_dom[me])
+      B[C_S1 * kLineWords + p] = ps.base[C_S1][p] + 1;  // the start round
   }
 }
 
@@ -773,6 +800,11 @@ struct ArOp {
   __device__ int peer(int i) const { return tp.members[tp.dom_first[k] + i]; }
   // offset of s2 in the slot of a rank whose domain has dq members
   __device__ size_t s2_off(int dq) const { return (size_t)(dq - 1) * (TL / dq); }
+  // domain peer i's data for tile offset c (in my region): its send buffer (pull) or my s1 slot (push)
+  __device__ const void* dsrc(int i, int slot, size_t tb, size_t c, size_t r0) const {
+    if (a.pull) return (const T*)a.peer_send[peer(i)] + tb + c;
+    return slot_ptr<T>(a, me, ch, slot) + (size_t)cidx(i, j) * Rk + (c - r0);
+  }
   // start of the region of owner o (domain q) within a tile, and o's Rk
   __device__ size_t region_lo(const Geo& g, int o) const {
     const int q = tp.rank_dom[o];
@@ -800,7 +832,7 @@ struct ArOp {
           if (c1 <= c0) continue;
           PtrList src, dst;
           for (int i = 0; i < d; i++)
-            src.add(i == j ? (const void*)(x + tb + c0) : (const void*)(mine + (size_t)cidx(i, j) * Rk + (c0 - r0)));
+            src.add(i == j ? (const void*)(x + tb + c0) : dsrc(i, slot, tb, c0, r0));
           if (D == 1) {
             dst.add(y + tb + c0);
           } else {
@@ -816,8 +848,7 @@ struct ArOp {
         const size_t c0 = g.piece(sg, k), c1 = g.piece(sg, k + 1);
         if (c1 <= c0) continue;
         PtrList inner, outer, dst;
-        for (int i = 0; i < d; i++)
-          inner.add(i == j ? (const void*)(x + tb + c0) : (const void*)(mine + (size_t)cidx(i, j) * Rk + (c0 - r0)));
+        for (int i = 0; i < d; i++) inner.add(i == j ? (const void*)(x + tb + c0) : dsrc(i, slot, tb, c0, r0));
         for (int q = 0; q < D; q++) outer.add(q == k ? nullptr : (const void*)(my_s2 + (size_t)q * Rk + (c0 - r0)));
         dst.add(y + tb + c0);
         for (int q = 0; q < D; q++) {

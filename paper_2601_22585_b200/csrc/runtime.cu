@@ -277,6 +277,31 @@ hetcclResult_t run_op(hetcclComm_t c, int op, const void* const* sends, void* co
   }
   // direct All-Reduce: stage E has no data, only its S3 wait (my y is complete) -> one end-of-kernel wait
   if (a.direct && env_long("HETCCL_FINAL_WAIT", 1)) a.final_stage = 4;
+  // pull: every rank's send buffer addressable too (mux, or sendbuf in a symmetric buffer at the same offset
+  // on every rank) -> the domain fold reads peers' x directly; stage A and its S1 handshake disappear
+  if (a.direct && env_long("HETCCL_PULL", 1)) {
+    if (c->kind == KIND_MUX) {
+      a.pull = 1;
+      for (int r = 0; r < c->n; r++) a.peer_send[r] = sends[r];
+    } else {
+      const char* x = (const char*)sends[0];
+      for (auto& b : c->sym)
+        if (b.connected && x >= b.base && x + count * (size_t)es <= b.base + b.bytes) {
+          a.pull = 1;
+          for (int r = 0; r < c->n; r++) a.peer_send[r] = (r == c->rank ? b.base : b.peer[r]) + (x - b.base);
+          break;
+        }
+    }
+    if (a.pull) {
+      a.active &= ~1u;  // no stage A
+      for (int r = 0; r < c->n; r++) {
+        a.rp[r].sig_ctr[0] = C_NONE;
+        a.rp[r].sig_mask[0] = 0;
+        a.rp[r].wait_ctr[1] = C_NONE;  // readiness is the start round instead
+        a.rp[r].wait_mask[1] = 0;
+      }
+    }
+  }
   {  // the ring must be deeper than the pipeline (plus the one-iteration release lag of the WS mode)
     int na = 0;
     for (int s = 0; s < kMaxStages; s++) na += (a.active >> s) & 1;
