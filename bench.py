@@ -281,10 +281,13 @@ def run_dist(args):
     count = args.mib * (1 << 20) // 2
     S = count * 2
     x = gen_inputs(1, count, first_rank=rank)[0]
-    send = torch.from_numpy(x.view(np.int16)).view(torch.bfloat16).to("cuda")
+    send_plain = torch.from_numpy(x.view(np.int16)).view(torch.bfloat16).to("cuda")
     comm = hc.init_process_group_comm(m)
-    # the gradient bucket's output lives in a symmetric buffer (hetccl_mem_*: same offset on every rank),
-    # so final pieces go straight into the peers' buffers; a plain torch buffer takes the staged path
+    # the gradient bucket and its output live in symmetric buffers (hetccl_mem_*: same offset on every
+    # rank): domain peers read x directly (pull) and final pieces go straight into the peers' buffers;
+    # plain torch buffers take the staged path (reported beside it)
+    send = hc.symmetric_empty(comm, count, torch.bfloat16)
+    send.copy_(send_plain)
     recv = hc.symmetric_empty(comm, count, torch.bfloat16)
     recv_staged = torch.empty_like(send)
     stream = torch.cuda.current_stream()
@@ -319,8 +322,8 @@ def run_dist(args):
         total_ms, launch_ms = timed(step, args.steps)
     # staged path (plain torch recv buffer) for comparison
     for _ in range(args.warmup):
-        hc.allreduce(send, recv_staged, comm, stream=sp)
-    staged_ms, _ = timed(lambda: hc.allreduce(send, recv_staged, comm, stream=sp), args.steps)
+        hc.allreduce(send_plain, recv_staged, comm, stream=sp)
+    staged_ms, _ = timed(lambda: hc.allreduce(send_plain, recv_staged, comm, stream=sp), args.steps)
     _, staged_bus = busbw(S, staged_ms / args.steps * 1e-3, world)
     hc.hetccl_comm_get_async_error(comm)
     t_step = total_ms / args.steps * 1e-3
@@ -371,7 +374,7 @@ def run_dist(args):
             "algbw": round(alg, 2), "gpu_launches": args.steps * world,
             "nccl_flat": {"busbw": round(nccl_bus, 2), "ratio": round(bus / nccl_bus, 4)},
             "staged_recv": {"busbw": round(staged_bus, 2),
-                            "note": "recv in a plain torch buffer: results staged through scratch (value: symmetric recv)"},
+                            "note": "send/recv in plain torch buffers: staged through scratch (value: symmetric buffers)"},
             "e2e": {"value": round(e2e_bus, 2), "unit": "GB/s", "h2d_bytes_per_step": world * S,
                     "d2h_bytes_per_step": world * S},
             "roofline": {"bound": "nvlink", "achieved": round(achieved, 1), "peak": NVLINK_PEAK, "unit": "GB/s",
