@@ -132,12 +132,16 @@ def main():
             it = 50
         t_staged = timed(lambda: hc.allreduce(x, y, c), it, graph=graph)
         ok = parity_ar(y, seed, count, m)
-        # symmetric recv buffer (hetccl_mem_*): results written straight into the peers' buffers
+        # symmetric send + recv buffers (hetccl_mem_*): peers' x read directly (pull), results written
+        # straight into the peers' buffers (direct)
+        xsym = hc.symmetric_empty(c, count, torch.bfloat16, group=gloo)
+        xsym.copy_(x)
         ysym = hc.symmetric_empty(c, count, torch.bfloat16, group=gloo)
-        t = timed(lambda: hc.allreduce(x, ysym, c), it, graph=graph)
+        t = timed(lambda: hc.allreduce(xsym, ysym, c), it, graph=graph)
         ok = ok and parity_ar(ysym, seed, count, m)
         hc.lib().hetccl_mem_free(c, ysym.data_ptr())
-        del ysym
+        hc.lib().hetccl_mem_free(c, xsym.data_ptr())
+        del ysym, xsym
         z = x.clone()
         tn = timed(lambda: dist.all_reduce(z), it, graph=graph)
         alg = S / t / 1e9
@@ -149,7 +153,7 @@ def main():
               "vs_nccl": round(bus / nbus, 4), "busbw_over_900": round(bus / 900, 4),
               "link_util_770": round(busiest / t / 1e9 / 770, 4), "r7_gate": ok, "cuda_graph": graph,
               "staged_busbw": round(S / t_staged / 1e9 * 2 * (world - 1) / world, 2),
-              "note": "busbw: recv in a symmetric buffer (direct); staged_busbw: plain torch recv buffer"})
+              "note": "busbw: send/recv in symmetric buffers (pull + direct); staged_busbw: plain torch buffers"})
         del x, y, z
 
     if args.what == "ar_sweep":
