@@ -279,7 +279,10 @@ hetcclResult_t run_op(hetcclComm_t c, int op, const void* const* sends, void* co
   if (a.direct && env_long("HETCCL_FINAL_WAIT", 1)) a.final_stage = 4;
   // pull: every rank's send buffer addressable too (mux, or sendbuf in a symmetric buffer at the same offset
   // on every rank) -> the domain fold reads peers' x directly; stage A and its S1 handshake disappear
-  if (a.direct && env_long("HETCCL_PULL", 1)) {
+  // HETCCL_PULL: 1 always, 0 never, unset = rank-multiplexed comms only (measured: mux +37%; one rank per GPU
+  // at 2+2 -10%, because plain 16-byte loads keep too few remote bytes in flight per CTA)
+  const long pull_env = env_long("HETCCL_PULL", -1);
+  if (a.direct && (pull_env == 1 || (pull_env < 0 && c->kind == KIND_MUX))) {
     if (c->kind == KIND_MUX) {
       a.pull = 1;
       for (int r = 0; r < c->n; r++) a.peer_send[r] = sends[r];
