@@ -181,6 +181,21 @@ __shared__ int g_dbase, g_dnth;
 constexpr int kUnroll = HETCCL_FOLD_UNROLL;      // vectors in flight per thread per source in a fold
 constexpr int kCopyUnroll = HETCCL_COPY_UNROLL;  // vectors in flight per thread in a copy
 
+#ifndef HETCCL_PREFETCH
+#define HETCCL_PREFETCH 2
+#endif
+// L2 prefetch, `HETCCL_PREFETCH` batches ahead, of the vectors a CTA-wide batch will load: one TMA bulk
+// prefetch per source issued by the first data thread (no registers, no shared memory). Hides the HBM
+// latency the register-bound loads cannot (128 threads x 4-8 vectors in flight per CTA).
+__device__ __forceinline__ void prefetch_ahead(const void* src, size_t v0, int tid, size_t batch_vecs, size_t nv) {
+  if (HETCCL_PREFETCH <= 0 || tid != 0) return;
+  const size_t vs = v0 + (size_t)HETCCL_PREFETCH * batch_vecs;
+  if (vs >= nv) return;
+  const size_t bytes = min(batch_vecs, nv - vs) * 16;
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"((const char*)src + vs * 16), "r"((uint32_t)bytes)
+               : "memory");
+}
+
 // dst[d][i] = src[i] for every destination d, i < n elements of size ES (bit copy)
 template <int ES>
 __device__ __noinline__ void cta_copy(const void* src, const PtrList& dsts, size_t n) {
@@ -192,6 +207,7 @@ __device__ __noinline__ void cta_copy(const void* src, const PtrList& dsts, size
   const size_t nv = all_aligned16(s1, dsts) ? n / V : 0;
   const char* sp = (const char*)src;
   for (size_t v0 = tid; v0 < nv; v0 += (size_t)kCopyUnroll * nth) {
+    prefetch_ahead(sp, v0, tid, (size_t)kCopyUnroll * nth, nv);
     uint4 w[kCopyUnroll];
 #pragma unroll
     for (int u = 0; u < kCopyUnroll; u++) {
@@ -240,6 +256,7 @@ __device__ __noinline__ void cta_fold(const PtrList& srcs, const PtrList& dsts, 
   const int tid = (int)threadIdx.x - g_dbase, nth = g_dnth;
   const size_t nv = all_aligned16(srcs, dsts) ? n / V : 0;
   for (size_t v0 = tid; v0 < nv; v0 += (size_t)kUnroll * nth) {
+    for (int s = 0; s < srcs.n; s++) prefetch_ahead(srcs.p[s], v0, tid, (size_t)kUnroll * nth, nv);
     A acc[kUnroll][V];
     {
       uint4 w[kUnroll];
@@ -318,6 +335,9 @@ __device__ __noinline__ void cta_fold_hier(const PtrList& inner, int kpos, const
     if (q != kpos) al |= (uintptr_t)outer.p[q];
   const size_t nv = (all_aligned16(inner, dsts) && (al & 15) == 0) ? n / V : 0;
   for (size_t v0 = tid; v0 < nv; v0 += (size_t)kUnroll * nth) {
+    for (int s = 0; s < inner.n; s++) prefetch_ahead(inner.p[s], v0, tid, (size_t)kUnroll * nth, nv);
+    for (int q = 0; q < D; q++)
+      if (q != kpos) prefetch_ahead(outer.p[q], v0, tid, (size_t)kUnroll * nth, nv);
     A acc[kUnroll][V];
     uint4 pk[kUnroll];
     // ---- inner fold -> P_kpos (narrowed, kept packed) ----
@@ -417,6 +437,7 @@ __device__ __forceinline__ void cta_fold_domains(const PtrList& srcs, const Topo
   const size_t nv = all_aligned16(srcs, dsts) ? n / V : 0;
   const int D = tp.D;
   for (size_t v0 = tid; v0 < nv; v0 += (size_t)kUnroll * nth) {
+    for (int s = 0; s < srcs.n; s++) prefetch_ahead(srcs.p[s], v0, tid, (size_t)kUnroll * nth, nv);
     A out[kUnroll][V], acc[kUnroll][V];
     for (int q = 0; q < D; q++) {
       const int d = tp.dom_size[q];
