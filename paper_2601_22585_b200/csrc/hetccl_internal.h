@@ -126,9 +126,10 @@ struct Geometry {
   size_t tile, ntiles;
   int nch;
 };
-Geometry make_geometry(const Topo& t, int op, size_t count, int es, int nch_max, size_t slot_elems);
+// tile_base: the per-rank All-Reduce tile in bytes (0 = 256 KiB); HETCCL_TILE_KB overrides it
+Geometry make_geometry(const Topo& t, int op, size_t count, int es, int nch_max, size_t slot_elems, size_t tile_base);
 size_t slot_mult_num(const Topo& t, int op, size_t tile);  // scratch elements one slot needs for `tile`
-size_t default_tile_bytes(int op, int n);                   // HETCCL_TILE_KB (AR/BC per rank; RS/AG per shard)
+size_t default_tile_bytes(int op, int n, size_t base);      // HETCCL_TILE_KB or base (AR/BC per rank; RS/AG per shard)
 size_t default_slot_bytes(const Topo& t, size_t tile_bytes);  // slot that fits every op's default tile
 int op_stages(int op);                                      // logical stages of op
 uint32_t active_stages(const Topo& t, int op, int root);   // active logical stages (same on all ranks)

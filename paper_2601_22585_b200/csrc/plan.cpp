@@ -104,14 +104,14 @@ size_t default_slot_bytes(const Topo& t, size_t tile_bytes) {
   return (need + 4095) / 4096 * 4096 + 65536;  // room for the quantum rounding of the tile
 }
 
-size_t default_tile_bytes(int op, int n) {
+size_t default_tile_bytes(int op, int n, size_t base) {
   const char* e = getenv("HETCCL_TILE_KB");
-  size_t b = e ? (size_t)atol(e) * 1024 : (size_t)256 * 1024;
+  size_t b = e ? (size_t)atol(e) * 1024 : (base ? base : (size_t)256 * 1024);
   if (op == OP_REDUCE_SCATTER || op == OP_ALL_GATHER || op == OP_ALL_TO_ALL) b /= (size_t)n;  // per shard / block
   return std::max<size_t>(b, 4096);
 }
 
-Geometry make_geometry(const Topo& t, int op, size_t count, int es, int nch_max, size_t slot_elems) {
+Geometry make_geometry(const Topo& t, int op, size_t count, int es, int nch_max, size_t slot_elems, size_t tile_base) {
   Geometry g{0, 0, 0};
   if (count == 0) return g;
   const int V = 16 / es;
@@ -134,7 +134,7 @@ Geometry make_geometry(const Topo& t, int op, size_t count, int es, int nch_max,
     }
     if (slot_mult_num(t, op, lo) <= slot_elems) cap = std::max(cap, lo);
   }
-  size_t target = std::max(q, floor_to(default_tile_bytes(op, t.n) / es, q));
+  size_t target = std::max(q, floor_to(default_tile_bytes(op, t.n, tile_base) / es, q));
   size_t tile = std::min(cap, target);
   // mid-size messages: shrink the tile (down to a floor) so every channel still gets a few tiles to
   // pipeline, instead of one tile walking all stages serially (HETCCL_MIN_TILES, HETCCL_TILE_FLOOR_KB)
