@@ -116,7 +116,6 @@ struct OpArgs {
                                 //   position; its work must be empty), or -1
   int direct;                   // 1: every rank's recv buffer is addressable here (peer_recv), so All-Reduce
   void* peer_recv[kMaxRanks];   //    writes final pieces straight into them (no staging through scratch)
-  int stage_remote;             // 1: remote fold sources (pull over NVLink) are staged in shared memory by TMA
   int pull;                     // 1 (with direct): every rank's send buffer is addressable (peer_send): the domain
   const void* peer_send[kMaxRanks];  // fold reads peers' x directly, stage A and the s1 staging vanish
 };

@@ -157,13 +157,8 @@ constexpr int kMaxList = kMaxRanks + 2;
 struct PtrList {
   const void* p[kMaxList];
   int n;
-  uint32_t remote;  // sources read over NVLink (staged through shared memory by TMA when g_staging)
-  __device__ PtrList() : n(0), remote(0) {}
+  __device__ PtrList() : n(0) {}
   __device__ void add(const void* q) { p[n++] = q; }
-  __device__ void add_remote(const void* q) {
-    remote |= 1u << n;
-    p[n++] = q;
-  }
 };
 
 __device__ __forceinline__ bool all_aligned16(const PtrList& a, const PtrList& b) {
@@ -176,42 +171,6 @@ __device__ __forceinline__ bool all_aligned16(const PtrList& a, const PtrList& b
 // data-thread geometry of the current CTA (set by run_pipeline: warp-specialised CTAs leave warp 0
 // to the flag protocol), read by the data movers
 __shared__ int g_dbase, g_dnth;
-
-// ---- TMA staging of remote fold sources (pull mode over NVLink) ----
-// Plain 16-byte loads keep ~8 KiB per CTA in flight, too little to cover NVLink latency; remote sources
-// of a fold are instead brought into a shared-memory ring by cp.async.bulk (one elected thread, mbarrier
-// completion), kStageRing batches ahead, and read from shared memory.
-constexpr int kStageRing = 3;
-constexpr int kMaxStaged = 3;  // remote sources per fold staged (more are read directly)
-__host__ __device__ constexpr size_t stage_batch_bytes(int unroll) { return (size_t)unroll * kThreads * 16; }
-__shared__ int g_staging;                      // dynamic shared memory holds the ring (set per launch)
-__shared__ __align__(8) uint64_t g_mbar[kStageRing];
-__shared__ uint32_t g_ring;                    // ring uses so far (stage = use % kStageRing, parity = use / ring)
-extern __shared__ __align__(128) char g_stage[];  // [kStageRing][kMaxStaged][batch]
-
-__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t ok = 0;
-  while (!ok)
-    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-                 : "=r"(ok) : "r"(smem_addr(bar)), "r"(parity) : "memory");
-}
-// thread 0: bring batch `b` (vectors [b*bv, b*bv + bv) of n) of every staged source into ring stage `st`
-__device__ __forceinline__ void stage_issue(const void* const* src, int ns, size_t b, size_t bv, size_t nv, int st) {
-  const size_t v0 = b * bv;
-  if (v0 >= nv) return;
-  const uint32_t bytes = (uint32_t)(min(bv, nv - v0) * 16);
-  uint64_t* bar = &g_mbar[st];
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes * (uint32_t)ns)
-               : "memory");
-  for (int i = 0; i < ns; i++) {
-    char* dst = g_stage + ((size_t)st * kMaxStaged + i) * bv * 16;
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_addr(dst)),
-                 "l"((const char*)src[i] + v0 * 16), "r"(bytes), "r"(smem_addr(bar))
-                 : "memory");
-  }
-}
 
 #ifndef HETCCL_FOLD_UNROLL
 #define HETCCL_FOLD_UNROLL 4
@@ -282,64 +241,6 @@ __device__ __forceinline__ void cta_copy1(const void* src, void* dst, size_t n) 
   cta_copy<ES>(src, d, n);
 }
 
-// Per-call staging plan of a fold's remote sources (pull mode, g_staging): batch b (kUnroll vectors per
-// thread, CTA-contiguous) of every staged source lands in ring stage (g_ring + b) % kStageRing.
-struct Staging {
-  bool on;
-  int nr;
-  uint32_t base;
-  size_t bv, nb, nv;
-  uint64_t rmap;  // 3 bits per source: 0 = read directly, i + 1 = staged as remote source i
-  const void* rs[kMaxStaged];
-  __device__ void init(const PtrList& l, size_t nv_, int nth, int tid) {
-    nv = nv_;
-    bv = (size_t)kUnroll * nth;
-    nb = (nv + bv - 1) / bv;
-    nr = 0;
-    on = g_staging && l.remote && nth == kThreads && nv > 0;
-    if (!on) return;
-    rmap = 0;
-    for (int s = 0; s < l.n; s++)
-      if (((l.remote >> s) & 1u) && nr < kMaxStaged) {
-        rmap |= (uint64_t)(nr + 1) << (3 * s);
-        rs[nr++] = l.p[s];
-      }
-    base = g_ring;
-    if (tid == 0) {
-      asm volatile("fence.proxy.async.global;" ::: "memory");  // peers' data was acquired in the generic proxy
-      for (size_t b = 0; b < nb && b < (size_t)kStageRing; b++) stage_issue(rs, nr, b, bv, nv, (int)((base + b) % kStageRing));
-    }
-  }
-  __device__ uint32_t wait(size_t b) const {
-    const uint32_t use = base + (uint32_t)b, st = use % kStageRing;
-    mbar_wait(&g_mbar[st], (use / kStageRing) & 1u);
-    return st;
-  }
-  __device__ const char* stage_of(int s, uint32_t st) const {
-    const int i = (int)((rmap >> (3 * s)) & 7u);
-    return i ? g_stage + ((size_t)st * kMaxStaged + (i - 1)) * bv * 16 : nullptr;
-  }
-  __device__ void release(size_t b, uint32_t st, int tid) const {
-    __syncthreads();  // every thread is done with stage st
-    if (tid == 0 && b + kStageRing < nb) stage_issue(rs, nr, b + kStageRing, bv, nv, (int)st);
-  }
-  __device__ void finish(int tid) const {
-    __syncthreads();
-    if (tid == 0) g_ring = base + (uint32_t)nb;
-    __syncthreads();
-  }
-};
-
-// kUnroll vectors of source s of a list for the batch starting at v0 (global, or the staged copy)
-__device__ __forceinline__ void load_batch(uint4 (&w)[kUnroll], const void* src, const char* staged, size_t v0, int tid,
-                                           int nth, size_t nv) {
-#pragma unroll
-  for (int u = 0; u < kUnroll; u++) {
-    const size_t v = v0 + (size_t)u * nth;
-    if (v < nv) w[u] = staged ? *(const uint4*)(staged + ((size_t)u * nth + tid) * 16) : ld_v4((const char*)src + v * 16);
-  }
-}
-
 // dst[d][i] = narrow( fold_{s in order} widen(src[s][i]) ) for every destination d
 template <typename T, int OP>
 __device__ __noinline__ void cta_fold(const PtrList& srcs, const PtrList& dsts, size_t n) {
@@ -348,31 +249,40 @@ __device__ __noinline__ void cta_fold(const PtrList& srcs, const PtrList& dsts, 
   using A = typename TR::A;
   constexpr int V = TR::V;
   if (n == 0) return;
-  if (srcs.n == 1 && !srcs.remote) {  // a single local operand: the value is already in the dtype (bit copy)
+  if (srcs.n == 1) {  // a single operand: the value is already in the dtype (bit copy)
     cta_copy<sizeof(S)>(srcs.p[0], dsts, n);
     return;
   }
   const int tid = (int)threadIdx.x - g_dbase, nth = g_dnth;
   const size_t nv = all_aligned16(srcs, dsts) ? n / V : 0;
-  Staging sg;
-  sg.init(srcs, nv, nth, tid);
-  for (size_t b = 0;; ++b) {
-    const size_t v0 = b * sg.bv + tid;
-    if (sg.on ? b >= sg.nb : v0 >= nv) break;
-    const uint32_t st = sg.on ? sg.wait(b) : 0;
-    if (!sg.on)
-      for (int s = 0; s < srcs.n; s++) prefetch_ahead(srcs.p[s], v0, tid, sg.bv, nv);
+  for (size_t v0 = tid; v0 < nv; v0 += (size_t)kUnroll * nth) {
+    for (int s = 0; s < srcs.n; s++) prefetch_ahead(srcs.p[s], v0, tid, (size_t)kUnroll * nth, nv);
     A acc[kUnroll][V];
-    for (int s = 0; s < srcs.n; s++) {
+    {
       uint4 w[kUnroll];
-      load_batch(w, srcs.p[s], sg.on ? sg.stage_of(s, st) : nullptr, v0, tid, nth, nv);
+      const char* sp = (const char*)srcs.p[0];
+#pragma unroll
+      for (int u = 0; u < kUnroll; u++) {
+        size_t v = v0 + (size_t)u * nth;
+        if (v < nv) w[u] = ld_v4(sp + v * 16);
+      }
 #pragma unroll
       for (int u = 0; u < kUnroll; u++)
 #pragma unroll
-        for (int e = 0; e < V; e++) {
-          const A x = TR::widen(Vec<S>::get(w[u], e));
-          acc[u][e] = s == 0 ? x : comb<OP>(acc[u][e], x);
-        }
+        for (int e = 0; e < V; e++) acc[u][e] = TR::widen(Vec<S>::get(w[u], e));
+    }
+    for (int s = 1; s < srcs.n; s++) {
+      uint4 w[kUnroll];
+      const char* sp = (const char*)srcs.p[s];
+#pragma unroll
+      for (int u = 0; u < kUnroll; u++) {
+        size_t v = v0 + (size_t)u * nth;
+        if (v < nv) w[u] = ld_v4(sp + v * 16);
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; u++)
+#pragma unroll
+        for (int e = 0; e < V; e++) acc[u][e] = comb<OP>(acc[u][e], TR::widen(Vec<S>::get(w[u], e)));
     }
     uint4 o[kUnroll];
 #pragma unroll
@@ -387,9 +297,7 @@ __device__ __noinline__ void cta_fold(const PtrList& srcs, const PtrList& dsts, 
         if (v < nv) st_v4(dp + v * 16, o[u]);
       }
     }
-    if (sg.on) sg.release(b, st, tid);
   }
-  if (sg.on) sg.finish(tid);
   for (size_t i = nv * V + tid; i < n; i += nth) {
     A a;
     if (sizeof(S) == 4) a = TR::widen((S)ld_s32((const char*)srcs.p[0] + i * 4));
@@ -411,7 +319,7 @@ __device__ __noinline__ void cta_fold(const PtrList& srcs, const PtrList& dsts, 
 //   dst[d][i] = narrow( fold_{q < outer.n in order} widen(P_q) ) for every destination d.
 // Used where a rank owns both its domain's partial and the cross-domain result of an element, so the
 // partial never round-trips through memory. Bitwise identical to cta_fold of inner, stored, then
-// cta_fold of outer. Remote inner sources (pull) are staged like cta_fold's.
+// cta_fold of outer.
 template <typename T, int OP>
 __device__ __noinline__ void cta_fold_hier(const PtrList& inner, int kpos, const PtrList& outer, const PtrList& dsts,
                                            size_t n) {
@@ -426,22 +334,21 @@ __device__ __noinline__ void cta_fold_hier(const PtrList& inner, int kpos, const
   for (int q = 0; q < D; q++)
     if (q != kpos) al |= (uintptr_t)outer.p[q];
   const size_t nv = (all_aligned16(inner, dsts) && (al & 15) == 0) ? n / V : 0;
-  Staging sg;
-  sg.init(inner, nv, nth, tid);
-  for (size_t b = 0;; ++b) {
-    const size_t v0 = b * sg.bv + tid;
-    if (sg.on ? b >= sg.nb : v0 >= nv) break;
-    const uint32_t st = sg.on ? sg.wait(b) : 0;
-    if (!sg.on)
-      for (int s = 0; s < inner.n; s++) prefetch_ahead(inner.p[s], v0, tid, sg.bv, nv);
+  for (size_t v0 = tid; v0 < nv; v0 += (size_t)kUnroll * nth) {
+    for (int s = 0; s < inner.n; s++) prefetch_ahead(inner.p[s], v0, tid, (size_t)kUnroll * nth, nv);
     for (int q = 0; q < D; q++)
-      if (q != kpos) prefetch_ahead(outer.p[q], v0, tid, sg.bv, nv);
+      if (q != kpos) prefetch_ahead(outer.p[q], v0, tid, (size_t)kUnroll * nth, nv);
     A acc[kUnroll][V];
     uint4 pk[kUnroll];
     // ---- inner fold -> P_kpos (narrowed, kept packed) ----
     for (int s = 0; s < inner.n; s++) {
       uint4 w[kUnroll];
-      load_batch(w, inner.p[s], sg.on ? sg.stage_of(s, st) : nullptr, v0, tid, nth, nv);
+      const char* sp = (const char*)inner.p[s];
+#pragma unroll
+      for (int u = 0; u < kUnroll; u++) {
+        size_t v = v0 + (size_t)u * nth;
+        if (v < nv) w[u] = ld_v4(sp + v * 16);
+      }
 #pragma unroll
       for (int u = 0; u < kUnroll; u++)
 #pragma unroll
@@ -467,7 +374,12 @@ __device__ __noinline__ void cta_fold_hier(const PtrList& inner, int kpos, const
         continue;
       }
       uint4 w[kUnroll];
-      load_batch(w, outer.p[q], nullptr, v0, tid, nth, nv);
+      const char* sp = (const char*)outer.p[q];
+#pragma unroll
+      for (int u = 0; u < kUnroll; u++) {
+        size_t v = v0 + (size_t)u * nth;
+        if (v < nv) w[u] = ld_v4(sp + v * 16);
+      }
 #pragma unroll
       for (int u = 0; u < kUnroll; u++)
 #pragma unroll
@@ -489,9 +401,7 @@ __device__ __noinline__ void cta_fold_hier(const PtrList& inner, int kpos, const
         if (v < nv) st_v4(dp + v * 16, o[u]);
       }
     }
-    if (sg.on) sg.release(b, st, tid);
   }
-  if (sg.on) sg.finish(tid);
   for (size_t i = nv * V + tid; i < n; i += nth) {
     A a = 0;
     for (int s = 0; s < inner.n; s++) {
@@ -755,13 +665,6 @@ __device__ __forceinline__ void run_pipeline(const OpArgs& a, Op& op, int me, in
   if (threadIdx.x == 0) {
     ps.tiles0 = B[kCounters * kLineWords];
     ps.abort_ = 0;
-    g_staging = a.stage_remote && !ws;
-    g_ring = 0;
-    if (g_staging) {
-      for (int i = 0; i < kStageRing; i++)
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&g_mbar[i])));
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
     g_dbase = ws ? 32 : 0;
     g_dnth = ws ? (int)blockDim.x - 32 : (int)blockDim.x;
   }
@@ -949,11 +852,8 @@ struct ArOp {
           const size_t c0 = g.piece(sg, q), c1 = g.piece(sg, q + 1);
           if (c1 <= c0) continue;
           PtrList src, dst;
-          for (int i = 0; i < d; i++) {
-            if (i == j) src.add(x + tb + c0);
-            else if (a.pull && g_staging) src.add_remote(dsrc(i, slot, tb, c0, r0));
-            else src.add(dsrc(i, slot, tb, c0, r0));
-          }
+          for (int i = 0; i < d; i++)
+            src.add(i == j ? (const void*)(x + tb + c0) : dsrc(i, slot, tb, c0, r0));
           if (D == 1) {
             dst.add(y + tb + c0);
           } else {
@@ -969,11 +869,7 @@ struct ArOp {
         const size_t c0 = g.piece(sg, k), c1 = g.piece(sg, k + 1);
         if (c1 <= c0) continue;
         PtrList inner, outer, dst;
-        for (int i = 0; i < d; i++) {
-          if (i == j) inner.add(x + tb + c0);
-          else if (a.pull && g_staging) inner.add_remote(dsrc(i, slot, tb, c0, r0));
-          else inner.add(dsrc(i, slot, tb, c0, r0));
-        }
+        for (int i = 0; i < d; i++) inner.add(i == j ? (const void*)(x + tb + c0) : dsrc(i, slot, tb, c0, r0));
         for (int q = 0; q < D; q++) outer.add(q == k ? nullptr : (const void*)(my_s2 + (size_t)q * Rk + (c0 - r0)));
         dst.add(y + tb + c0);
         for (int q = 0; q < D; q++) {
@@ -1474,7 +1370,6 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_allreduce_oneshot(cons
     abort_ = 0;
     g_dbase = 0;
     g_dnth = blockDim.x;
-    g_staging = 0;
   }
   __syncthreads();
   const unsigned long long g = ops0;
@@ -1613,14 +1508,8 @@ cudaError_t launch_collective(const OpArgs& a, int nlocal, int dt, int red, bool
   if (!fn) return cudaErrorInvalidValue;
   dim3 grid(a.nch, nlocal), block(kThreads);
   void* args[] = {(void*)&a};
-  size_t smem = 0;
-  if (a.stage_remote) {  // the TMA staging ring of remote fold sources (dynamic shared memory)
-    smem = (size_t)kStageRing * kMaxStaged * stage_batch_bytes(kUnroll);
-    cudaError_t e = cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-  }
-  if (cooperative) return cudaLaunchCooperativeKernel((const void*)fn, grid, block, args, smem, s);
-  return cudaLaunchKernel((const void*)fn, grid, block, args, smem, s);
+  if (cooperative) return cudaLaunchCooperativeKernel((const void*)fn, grid, block, args, 0, s);
+  return cudaLaunchKernel((const void*)fn, grid, block, args, 0, s);
 }
 
 cudaError_t launch_copy(const void* src, void* dst, size_t n, int es, cudaStream_t s) {

@@ -297,8 +297,6 @@ hetcclResult_t run_op(hetcclComm_t c, int op, const void* const* sends, void* co
         }
     }
     if (a.pull) {
-      // peers' x comes over NVLink: stage it through shared memory with TMA (HETCCL_STAGE=0 disables)
-      a.stage_remote = c->kind != KIND_MUX && env_long("HETCCL_STAGE", 1) != 0 && c->ws < 2;
       a.active &= ~1u;  // no stage A
       for (int r = 0; r < c->n; r++) {
         a.rp[r].sig_ctr[0] = C_NONE;
