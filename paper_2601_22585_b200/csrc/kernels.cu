@@ -171,6 +171,7 @@ __device__ __forceinline__ bool all_aligned16(const PtrList& a, const PtrList& b
 // data-thread geometry of the current CTA (set by run_pipeline: warp-specialised CTAs leave warp 0
 // to the flag protocol), read by the data movers
 __shared__ int g_dbase, g_dnth;
+__shared__ int g_pf;  // 1: the movers may L2-prefetch their sources (all local); 0 when folds read peers' memory
 
 #ifndef HETCCL_FOLD_UNROLL
 #define HETCCL_FOLD_UNROLL 4
@@ -188,7 +189,7 @@ constexpr int kCopyUnroll = HETCCL_COPY_UNROLL;  // vectors in flight per thread
 // prefetch per source issued by the first data thread (no registers, no shared memory). Hides the HBM
 // latency the register-bound loads cannot (128 threads x 4-8 vectors in flight per CTA).
 __device__ __forceinline__ void prefetch_ahead(const void* src, size_t v0, int tid, size_t batch_vecs, size_t nv) {
-  if (HETCCL_PREFETCH <= 0 || tid != 0) return;
+  if (HETCCL_PREFETCH <= 0 || tid != 0 || !g_pf) return;  // (a bulk prefetch of peer memory stalls ~20x)
   const size_t vs = v0 + (size_t)HETCCL_PREFETCH * batch_vecs;
   if (vs >= nv) return;
   const size_t bytes = min(batch_vecs, nv - vs) * 16;
@@ -665,6 +666,7 @@ __device__ __forceinline__ void run_pipeline(const OpArgs& a, Op& op, int me, in
   if (threadIdx.x == 0) {
     ps.tiles0 = B[kCounters * kLineWords];
     ps.abort_ = 0;
+    g_pf = !a.remote_pull;
     g_dbase = ws ? 32 : 0;
     g_dnth = ws ? (int)blockDim.x - 32 : (int)blockDim.x;
   }
@@ -1370,6 +1372,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_allreduce_oneshot(cons
     abort_ = 0;
     g_dbase = 0;
     g_dnth = blockDim.x;
+    g_pf = 1;
   }
   __syncthreads();
   const unsigned long long g = ops0;

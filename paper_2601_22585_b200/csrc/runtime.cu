@@ -297,6 +297,7 @@ hetcclResult_t run_op(hetcclComm_t c, int op, const void* const* sends, void* co
         }
     }
     if (a.pull) {
+      a.remote_pull = c->kind != KIND_MUX;
       a.active &= ~1u;  // no stage A
       for (int r = 0; r < c->n; r++) {
         a.rp[r].sig_ctr[0] = C_NONE;
