@@ -62,6 +62,22 @@ def test_null_and_bad_args_without_gpu(hc):
     assert lib.hetccl_plan_info(2, hc._imap([0, 1]), 0, 9, 16, 9, 0, 0, ctypes.byref(info)) == 4  # bad op
     assert lib.hetccl_plan_info(2, hc._imap([0, 1]), 0, 0, 16, 5, 0, 0, ctypes.byref(info)) == 4  # bad dtype
     assert lib.hetccl_plan_info(2, hc._imap([0, 1]), 0, 3, 16, 9, 2, 0, ctypes.byref(info)) == 4  # bad root
+    assert lib.hetccl_plan_info(2, hc._imap([0, 1]), 0, 4, 16, 9, 5, 0, ctypes.byref(info)) == 4  # reduce: bad root
+    # every entry point rejects a null communicator with hetcclInvalidArgument (no CUDA needed)
+    p = ctypes.c_void_p()
+    assert lib.hetccl_reduce(None, None, 4, 9, 0, 0, None, None) == 4
+    assert lib.hetccl_all_to_all(None, None, 4, 9, None, None) == 4
+    assert lib.hetccl_reduce_scatter(None, None, 4, 9, 0, None, None) == 4
+    assert lib.hetccl_all_gather(None, None, 4, 9, None, None) == 4
+    assert lib.hetccl_broadcast(None, None, 4, 9, 0, None, None) == 4
+    assert lib.hetccl_mem_alloc(None, 1024, ctypes.byref(p)) == 4
+    assert lib.hetccl_mem_free(None, None) == 4
+    assert lib.hetccl_mem_connect(None, None, None, 0) == 4
+    assert lib.hetccl_comm_destroy(None) == 4
+    assert lib.hetccl_comm_get_async_error(None) == 4
+    shape = (ctypes.c_int * 3)()
+    assert lib.hetccl_comm_get_trace(None, None, 0, shape) == 4
+    assert lib.hetccl_get_last_error(None) == b"null comm"
 
 
 SPLITS = {"1+1": [0, 1], "2+2": [0, 0, 1, 1], "1+3": [0, 1, 1, 1], "1+1+2": [0, 1, 2, 2],
