@@ -117,6 +117,7 @@ struct OpArgs {
   int direct;                   // 1: every rank's recv buffer is addressable here (peer_recv), so All-Reduce
   void* peer_recv[kMaxRanks];   //    writes final pieces straight into them (no staging through scratch)
   int remote_pull;              // 1: pull sources are peers' memory over NVLink (no L2 bulk prefetch of those)
+  int flat_ag;                  // 1 (with direct): C writes each final piece into EVERY rank's recv (no stage D)
   int pull;                     // 1 (with direct): every rank's send buffer is addressable (peer_send): the domain
   const void* peer_send[kMaxRanks];  // fold reads peers' x directly, stage A and the s1 staging vanish
 };

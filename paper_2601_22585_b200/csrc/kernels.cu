@@ -878,6 +878,10 @@ struct ArOp {
           if (q == k) continue;
           const int o = owner_of(tp, q, sg);
           const int dq = tp.dom_size[q];
+          if (a.flat_ag) {  // every member of domain q, not only the segment's owner (no forwarding stage D)
+            for (int i = 0; i < dq; i++) dst.add((T*)a.peer_recv[tp.members[tp.dom_first[q] + i]] + tb + c0);
+            continue;
+          }
           if (a.direct) dst.add((T*)a.peer_recv[o] + tb + c0);  // straight into the owner's recv buffer
           else dst.add(slot_ptr<T>(a, o, ch, slot) + s2_off(dq) + (size_t)D * (TL / dq) + (c0 - region_lo(g, o)));
         }

@@ -278,6 +278,26 @@ hetcclResult_t run_op(hetcclComm_t c, int op, const void* const* sends, void* co
   }
   // direct All-Reduce: stage E has no data, only its S3 wait (my y is complete) -> one end-of-kernel wait
   if (a.direct && env_long("HETCCL_FINAL_WAIT", 1)) a.final_stage = 4;
+  // HETCCL_FLAT_AG=1 (opt-in, direct only): the cross-domain all-gather delivers each final piece to every
+  // member of the other domains instead of their segment owner, so the intra-domain forwarding stage D
+  // disappears. Same NVLink bytes per rank, more of them cross domains (the paper's hierarchy minimises
+  // those): a deviation for NVSwitch, off by default.
+  if (a.direct && a.final_stage == 4 && c->topo.D > 1 && env_long("HETCCL_FLAT_AG", 0) == 1) {
+    a.flat_ag = 1;
+    a.active &= ~(1u << 3);
+    for (int r = 0; r < c->n; r++) {
+      const uint32_t all = ((1u << c->n) - 1u) & ~(1u << r);
+      a.rp[r].sig_ctr[2] = C_S3;  // C signals every rank; the end-of-kernel wait collects them
+      a.rp[r].sig_mask[2] = (uint16_t)all;
+      a.rp[r].wait_ctr[3] = C_NONE;
+      a.rp[r].wait_mask[3] = 0;
+      a.rp[r].sig_ctr[3] = C_NONE;
+      a.rp[r].sig_mask[3] = 0;
+      a.rp[r].wait_ctr[4] = C_S3;
+      a.rp[r].wait_mask[4] = (uint16_t)all;
+      a.rp[r].writes |= (uint16_t)all;
+    }
+  }
   // pull: every rank's send buffer addressable too (mux, or sendbuf in a symmetric buffer at the same offset
   // on every rank) -> the domain fold reads peers' x directly; stage A and its S1 handshake disappear
   // HETCCL_PULL: 1 always, 0 never, unset = rank-multiplexed comms only (measured: mux +37%; one rank per GPU

@@ -95,8 +95,8 @@ def test_c1_fp32_1mi_bitexact():
 
 
 @pytest.mark.parametrize("name", ["1+1", "2+2", "1+3", "1+1+2", "4"])
-@pytest.mark.parametrize("inplace,pull", [(False, "-1"), (True, "-1"), (True, "1")])
-def test_allreduce_symmetric_direct(name, inplace, pull, monkeypatch):
+@pytest.mark.parametrize("inplace,pull,flat", [(False, "-1", "0"), (True, "-1", "0"), (True, "1", "0"), (False, "-1", "1")])
+def test_allreduce_symmetric_direct(name, inplace, pull, flat, monkeypatch):
     """Symmetric recv buffers (hetccl_mem_*): final pieces are written straight into the peers' buffers;
     results bitwise equal to the oracle, at an offset inside the buffer, in and out of place."""
     import torch
@@ -108,6 +108,7 @@ def test_allreduce_symmetric_direct(name, inplace, pull, monkeypatch):
     monkeypatch.setenv("HETCCL_TILE_KB", "16")
     monkeypatch.setenv("HETCCL_ONESHOT_KB", "0")
     monkeypatch.setenv("HETCCL_PULL", pull)  # in place: the send buffer is symmetric too, so 1 = pull mode
+    monkeypatch.setenv("HETCCL_FLAT_AG", flat)
     count, off = 5 * 8192 + 333, 1000
     xs = inputs("normal", 17, n, count, "bf16")
     comms = _comms(m)

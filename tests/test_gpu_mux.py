@@ -172,13 +172,15 @@ def test_cuda_graph_replay(monkeypatch):
         hc.hetccl_comm_destroy(comm)
 
 
-@pytest.mark.parametrize("direct,final_wait,pull", [("0", "1", "0"), ("1", "0", "0"), ("1", "1", "0"), ("1", "1", "1")])
+@pytest.mark.parametrize("direct,final_wait,pull,flat", [("0", "1", "0", "0"), ("1", "0", "0", "0"), ("1", "1", "0", "0"),
+                                                        ("1", "1", "1", "0"), ("1", "1", "0", "1"), ("1", "1", "1", "1")])
 @pytest.mark.parametrize("name", ["2+2", "1+3", "4+4", "2+6", "2+2+4", "8", "1+1"])
-def test_allreduce_direct_and_staged(name, direct, final_wait, pull, monkeypatch):
+def test_allreduce_direct_and_staged(name, direct, final_wait, pull, flat, monkeypatch):
     """Rank-multiplexed comms write final pieces straight into every rank's recv buffer (HETCCL_DIRECT=1,
     default) — in place too; HETCCL_DIRECT=0 keeps the staged path of the multi-GPU mode."""
     monkeypatch.setenv("HETCCL_DIRECT", direct)
     monkeypatch.setenv("HETCCL_FINAL_WAIT", final_wait)
     monkeypatch.setenv("HETCCL_PULL", pull)
+    monkeypatch.setenv("HETCCL_FLAT_AG", flat)
     _run_ar(name, "bf16", "sum", 70001, tile_kb=16, monkeypatch=monkeypatch)
     _run_ar(name, "f32", "sum", 50021, tile_kb=16, inplace=True, monkeypatch=monkeypatch)
