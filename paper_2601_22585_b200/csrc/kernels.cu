@@ -1,28 +1,32 @@
-// kernels.cu — sm_100a device code of the hierarchical collectives (SURVEY.md §8(a) a1-a9).
+// kernels.cu — sm_100a device code of the hierarchical collectives (SURVEY.md §8(a) a1-a9, §8(f)).
 //
-// One persistent CTA per (channel, local rank). Every op is a short list of stages (All-Reduce:
-// A intra push, B intra fold + cross push, C cross fold + AG push, D final region -> y and domain
-// peers, E peers' regions -> y); a channel runs them as a SOFTWARE PIPELINE over its tiles
-// t = ch, ch+nch, ...: iteration i runs stage at position p on the channel's tile i-p, so the
-// intra-domain and cross-domain stages of different tiles overlap and no flag round trip sits on
-// the critical path (run_pipeline). Data moves with 16-byte vector loads/stores; remote stores go
-// straight into a peer's IPC-mapped scratch slot over NVLink 5 / NVSwitch ("push"), all loads are
-// local. Hand-off between stages uses per-(receiver, channel, counter, SENDER) counters:
+// One persistent CTA per (channel, local rank), 128 threads, two CTAs per SM. Every op is a short list
+// of stages (All-Reduce: A intra push, B domain fold of the other domains' pieces + cross push, C
+// domain fold of my pieces + cross fold + all-gather writes, D intra forward, E completion); a channel
+// runs them as a SOFTWARE PIPELINE over its tiles t = ch, ch+nch, ...: iteration i runs the stage at
+// position p on the channel's tile i-p, so the intra- and cross-domain stages of different tiles overlap
+// and no flag round trip sits on the critical path (run_pipeline). Data moves with 16-byte vector
+// loads/stores (plus an L2 bulk prefetch of the next batches); stores go straight into a peer's
+// IPC-mapped scratch slot, or — when every rank's recv buffer is addressable (rank-multiplexed comms,
+// symmetric buffers) — straight into the peers' recv buffers ("direct"), and the domain fold may read
+// the peers' send buffers ("pull", rank-multiplexed comms). Hand-off between stages uses per-(receiver,
+// channel, counter, SENDER) counters:
 //   writer: data stores -> __syncthreads -> fence.acq_rel.sys -> red.relaxed.sys.add(+1) on the
 //           receiver's counter word of this sender;
 //   reader: lane p of warp 0 spins ld.acquire.sys on sender p's word until it reaches the
-//           cumulative target -> __syncthreads -> ld.global.cg of the staged data.
+//           cumulative target -> __syncthreads -> loads of the data.
 // Scratch is a ring of nslots slots per channel indexed by the channel's cumulative tile count;
 // before writing a tile's slot a rank waits for the ACK of the tile that last used it. Targets are
 // cumulative across launches (kept in the rank's own base lines), so the protocol needs no host
 // sequence numbers and replays under CUDA graphs. The same kernels serve the rank-multiplexed mode
 // (all ranks on one device, rank = blockIdx.y, cooperative launch) and the one-rank-per-GPU mode.
+// Small All-Reduces take k_allreduce_oneshot (one push round, local domain-major reduction).
 //
 // Arithmetic (readings R3, R5, R6, R8): per element, fold ascending rank inside a domain
-// (seeded with the first operand), narrow 16-bit types once at the domain boundary (stored partial),
-// fold the D partials in ascending domain id, narrow once more. fp32 accumulation for bf16/fp16,
-// IEEE RNE everywhere (__fadd_rn, __float2bfloat16_rn, __float2half_rn), uint32 wrap for int32.
-// Built without --use_fast_math (no FTZ, reading R9).
+// (seeded with the first operand), narrow 16-bit types once at the domain boundary, fold the D
+// partials in ascending domain id, narrow once more. fp32 accumulation for bf16/fp16, IEEE RNE
+// everywhere (__fadd_rn, __float2bfloat16_rn, __float2half_rn), uint32 wrap for int32. Built
+// without --use_fast_math (no FTZ, reading R9).
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
