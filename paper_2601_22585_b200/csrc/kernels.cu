@@ -582,25 +582,27 @@ struct Pipe {
     return tl >= 0 && tl < ntl;
   }
   // sync warp: wait for everything iteration `it` needs; false on timeout
+  // (position, sender) pairs are spread over the warp's lanes, so every counter of the iteration is read
+  // in parallel (one flag round trip per iteration, not one per position)
   __device__ bool poll(long long it) {
     bool ok = true;
-    if (lane >= n) return true;
-    for (int p = 0; p < npos && ok; p++) {
+    for (int idx = lane; idx < npos * n && ok; idx += 32) {
+      const int p = idx / n, snd = idx % n;
       long long tl;
       if (stage_at[p] < 0 || !tile_at(it, p, tl)) continue;
       const int s = stage_at[p];
       const uint64_t* w1 = nullptr;
       uint64_t t1 = 0;
-      if (p == 0 && ((rp.writes >> lane) & 1u) && tiles0 + tl >= (unsigned long long)a.nslots) {
-        w1 = F + C_ACK * kLineWords + lane;
+      if (p == 0 && ((rp.writes >> snd) & 1u) && tiles0 + tl >= (unsigned long long)a.nslots) {
+        w1 = F + C_ACK * kLineWords + snd;
         t1 = tiles0 + tl - a.nslots + 1;
       }
       const int wc = rp.wait_ctr[s];
       const uint64_t* w2 = nullptr;
       uint64_t t2 = 0;
-      if (wc != C_NONE && ((rp.wait_mask[s] >> lane) & 1u)) {
-        w2 = F + wc * kLineWords + lane;
-        t2 = ps.base[wc][lane] + tl + 1;
+      if (wc != C_NONE && ((rp.wait_mask[s] >> snd) & 1u)) {
+        w2 = F + wc * kLineWords + snd;
+        t2 = ps.base[wc][snd] + tl + 1;
       }
       for (int q = 0; q < 2 && ok; q++) {
         const uint64_t* w = q ? w2 : w1;
@@ -610,7 +612,7 @@ struct Pipe {
         uint32_t spins = 0;
         while (ld_acquire_sys(w) < tg) {
           if ((++spins & 1023u) == 0 && (long long)(globaltimer() - t0) > a.timeout_ns) {
-            atomicOr(a.err, 1ull + ((unsigned long long)(q ? wc : C_ACK) << 8) + ((unsigned long long)lane << 16));
+            atomicOr(a.err, 1ull + ((unsigned long long)(q ? wc : C_ACK) << 8) + ((unsigned long long)snd << 16));
             ok = false;
             break;
           }
