@@ -137,3 +137,45 @@ def test_allreduce_symmetric_direct(name, inplace, pull, flat, monkeypatch):
     finally:
         for c in comms:
             hc.hetccl_comm_destroy(c)
+
+
+def test_two_comms_two_streams_concurrently(monkeypatch):
+    """C4's pattern: independent All-Reduces on two streams, one communicator per stream, channel counts
+    that fit the SMs together (148 + 148 of 296 co-resident CTAs); results bitwise equal to the oracle."""
+    import torch
+    import paper_2601_22585_b200 as hc
+    m = MAPS["2+2"] if _ngpu() >= 4 else MAPS["1+1"]
+    n = len(m)
+    if _ngpu() < n:
+        pytest.skip(f"needs {n} GPUs")
+    monkeypatch.setenv("HETCCL_NCHANNELS", "148")
+    monkeypatch.setenv("HETCCL_ONESHOT_KB", "0")
+    monkeypatch.setenv("HETCCL_TILE_KB", "64")
+    ca = hc.hetccl_comm_init_all(list(range(n)), m)
+    cb = hc.hetccl_comm_init_all(list(range(n)), m)
+    try:
+        count = 3 * (1 << 20) + 11
+        xa = inputs("normal", 61, n, count, "bf16")
+        xb = inputs("normal", 62, n, count, "bf16")
+        sa = [torch.cuda.Stream(device=r) for r in range(n)]
+        sb = [torch.cuda.Stream(device=r) for r in range(n)]
+        ta = [to_torch(xa[r], "bf16", f"cuda:{r}") for r in range(n)]
+        tb = [to_torch(xb[r], "bf16", f"cuda:{r}") for r in range(n)]
+        ya = [torch.empty_like(t) for t in ta]
+        yb = [torch.empty_like(t) for t in tb]
+        _sync(n)
+        for it in range(4):
+            for r in range(n):
+                hc.allreduce(ta[r], ya[r], ca[r], stream=sa[r])
+                hc.allreduce(tb[r], yb[r], cb[r], stream=sb[r])
+        _sync(n)
+        wa = oracle.allreduce(xa, m, "bf16", "sum")
+        wb = oracle.allreduce(xb, m, "bf16", "sum")
+        for r in range(n):
+            hc.hetccl_comm_get_async_error(ca[r])
+            hc.hetccl_comm_get_async_error(cb[r])
+            assert np.array_equal(to_numpy(ya[r], "bf16"), wa), f"stream a rank {r}"
+            assert np.array_equal(to_numpy(yb[r], "bf16"), wb), f"stream b rank {r}"
+    finally:
+        for c in ca + cb:
+            hc.hetccl_comm_destroy(c)
