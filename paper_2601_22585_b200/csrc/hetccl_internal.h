@@ -134,6 +134,7 @@ size_t slot_mult_num(const Topo& t, int op, size_t tile);  // scratch elements o
 size_t default_tile_bytes(int op, int n, size_t base);      // HETCCL_TILE_KB or base (AR/BC per rank; RS/AG per shard)
 size_t default_slot_bytes(const Topo& t, size_t tile_bytes);  // slot that fits every op's default tile
 int op_stages(int op);                                      // logical stages of op
+int bcast_relay(const Topo& t, int root);                   // Broadcast: member taking the root's share, or -1
 uint32_t active_stages(const Topo& t, int op, int root);   // active logical stages (same on all ranks)
 void make_rank_plan(const Topo& t, int op, int rank, int root, RankPlan* rp);
 void plan_bytes(const Topo& t, int op, int rank, int root, size_t count, int es, size_t tile, size_t* sent,

@@ -1148,47 +1148,77 @@ struct BcOp {
     is_root = (me == root);
   }
   __device__ int peer(int i) const { return tp.members[tp.dom_first[k] + i]; }
+  // the member of the root's domain that takes over the root's region (plan.cpp bcast_relay), or -1
+  __device__ int relay() const {
+    const int dr = tp.dom_size[kr];
+    return dr < 2 ? -1 : tp.members[tp.dom_first[kr] + (tp.rank_idx[root] + 1) % dr];
+  }
   __device__ void stage(int s, size_t t, int slot) {
     const size_t tb = t * TL, len = min(TL, a.count - tb);
     const Geo g{len, TL, L, 1};
     T* mine = slot_ptr<T>(a, me, ch, slot);
     const size_t r0 = g.seg(s_lo), r1 = g.seg(s_hi);
     const T* myreg = is_root ? (x + tb + r0) : mine;
-    if (s == 0) {  // ---- A: the root scatters the regions of its domain ----
+    const int rl = relay(), rj = tp.rank_idx[root];
+    const bool am_relay = (me == rl);
+    // the root's region as the relay holds it: my s3 entry for the root (filled by the root in A)
+    const T* rootreg = am_relay ? mine + Rk + (size_t)cidx(rj, j) * Rk : nullptr;
+    const size_t q0 = g.seg(rj * spj), q1 = g.seg((rj + 1) * spj);  // root's region (in its domain)
+    if (s == 0) {  // ---- A: the root scatters the regions of its domain (its own to the relay) ----
       if (!is_root) return;
       for (int i = 0; i < d; i++) {
         if (i == j) continue;
         const size_t p0 = g.seg(i * spj), p1 = g.seg((i + 1) * spj);
         cta_copy1<ES>(x + tb + p0, slot_ptr<T>(a, peer(i), ch, slot), p1 - p0);
+        if (peer(i) == rl) cta_copy1<ES>(x + tb + r0, slot_ptr<T>(a, rl, ch, slot) + Rk + (size_t)cidx(j, i) * Rk, r1 - r0);
       }
-    } else if (s == 1) {  // ---- B: root-domain owners send each segment to its owner in every other domain ----
-      if (k != kr) return;
-      for (int sg = s_lo; sg < s_hi; sg++) {
-        const size_t c0 = g.seg(sg), c1 = g.seg(sg + 1);
-        PtrList dst;
-        for (int q = 0; q < D; q++) {
-          if (q == kr) continue;
-          const int o = owner_of(tp, q, sg);
-          const size_t ro = g.seg(tp.rank_idx[o] * (L / tp.dom_size[q]));
-          dst.add(slot_ptr<T>(a, o, ch, slot) + (c0 - ro));
+    } else if (s == 1) {  // ---- B: each root-domain segment to its owner in every other domain ----
+      if (k != kr || (is_root && rl >= 0)) return;
+      for (int pass = 0; pass < (am_relay ? 2 : 1); pass++) {
+        const int lo = pass ? rj * spj : s_lo, hi = pass ? (rj + 1) * spj : s_hi;
+        const T* src = pass ? rootreg : myreg;
+        const size_t base = pass ? q0 : r0;
+        for (int sg = lo; sg < hi; sg++) {
+          const size_t c0 = g.seg(sg), c1 = g.seg(sg + 1);
+          PtrList dst;
+          for (int q = 0; q < D; q++) {
+            if (q == kr) continue;
+            const int o = owner_of(tp, q, sg);
+            const size_t ro = g.seg(tp.rank_idx[o] * (L / tp.dom_size[q]));
+            dst.add(slot_ptr<T>(a, o, ch, slot) + (c0 - ro));
+          }
+          cta_copy<ES>(src + (c0 - base), dst, c1 - c0);
         }
-        cta_copy<ES>(myreg + (c0 - r0), dst, c1 - c0);
       }
-    } else if (s == 2) {  // ---- C: my region -> y and every domain peer but the root ----
+    } else if (s == 2) {  // ---- C: my region (and the relay: the root's) -> y and every peer but the root ----
+      if (is_root) {
+        if (x != y) cta_copy1<ES>(x + tb, y + tb, len);
+        return;
+      }
       PtrList dst;
-      if (!is_root) dst.add(y + tb + r0);
+      dst.add(y + tb + r0);
       for (int i = 0; i < d; i++) {
         if (i == j) continue;
         const int pr = peer(i);
         if (pr == root) continue;
         dst.add(slot_ptr<T>(a, pr, ch, slot) + Rk + (size_t)cidx(j, i) * Rk);
       }
-      if (dst.n) cta_copy<ES>(myreg, dst, r1 - r0);
-      if (is_root && x != y) cta_copy1<ES>(x + tb, y + tb, len);
-    } else {  // ---- D: domain peers' regions -> y ----
+      cta_copy<ES>(myreg, dst, r1 - r0);
+      if (am_relay) {
+        PtrList dr;
+        dr.add(y + tb + q0);
+        for (int i = 0; i < d; i++) {
+          if (i == j) continue;
+          const int pr = peer(i);
+          if (pr == root) continue;
+          dr.add(slot_ptr<T>(a, pr, ch, slot) + Rk + (size_t)cidx(rj, i) * Rk);
+        }
+        cta_copy<ES>(rootreg, dr, q1 - q0);
+      }
+    } else {  // ---- D: domain peers' regions (the root's via the relay) -> y ----
       if (is_root) return;
       for (int i = 0; i < d; i++) {
-        if (i == j) continue;
+        if (i == j || (am_relay && i == rj && k == kr)) continue;
         const size_t p0 = g.seg(i * spj), p1 = g.seg((i + 1) * spj);
         cta_copy1<ES>(mine + Rk + (size_t)cidx(i, j) * Rk, y + tb + p0, p1 - p0);
       }

@@ -154,6 +154,12 @@ Geometry make_geometry(const Topo& t, int op, size_t count, int es, int nch_max,
   return g;
 }
 
+int bcast_relay(const Topo& t, int root) {  // -1 if the root is alone in its domain
+  const int kr = t.rank_dom[root], d = t.dom_size[kr];
+  if (d < 2) return -1;
+  return t.members[t.dom_first[kr] + (t.rank_idx[root] + 1) % d];
+}
+
 static int owner_of(const Topo& t, int q, int s) {  // domain q's owner of elementary segment s
   int dq = t.dom_size[q];
   return t.members[t.dom_first[q] + s / (t.L / dq)];
@@ -213,22 +219,36 @@ static int op_spec(const Topo& t, int op, int rank, int root, StageSpec st[kMaxS
       st[2] = {any_intra, C_S1, dpeers, C_NONE, 0};
       return 3;
     case OP_BROADCAST: {
+      // The root's port is the bound, so with a domain peer available the root only scatters (its own
+      // region goes to the RELAY, the next member of its domain, who then does the root's share of the
+      // cross push and of the intra all-gather): root egress T per tile instead of up to 2T.
       const int kr = t.rank_dom[root];
       const bool in_root_dom = (k == kr), is_root = (rank == root);
+      const int relay = bcast_relay(t, root);
       uint32_t bcross = 0;
-      for (int s = j * spj; s < (j + 1) * spj; s++) {
-        if (in_root_dom) {
-          for (int q = 0; q < D; q++)
-            if (q != kr) bcross |= 1u << owner_of(t, q, s);
-        } else {
-          bcross |= 1u << owner_of(t, kr, s);
+      auto cross_of = [&](int s) {  // other domains' owners of root-domain segment s
+        for (int q = 0; q < D; q++)
+          if (q != kr) bcross |= 1u << owner_of(t, q, s);
+      };
+      if (in_root_dom && !is_root) {
+        for (int s = j * spj; s < (j + 1) * spj; s++) cross_of(s);
+        if (rank == relay) {
+          const int rj = t.rank_idx[root];
+          for (int s = rj * spj; s < (rj + 1) * spj; s++) cross_of(s);
+        }
+      } else if (in_root_dom && relay < 0) {  // the root is alone in its domain: it pushes cross itself
+        for (int s = j * spj; s < (j + 1) * spj; s++) cross_of(s);
+      } else if (!in_root_dom) {
+        for (int s = j * spj; s < (j + 1) * spj; s++) {
+          const int o = owner_of(t, kr, s);
+          bcross |= 1u << (o == root && relay >= 0 ? relay : o);
         }
       }
       const uint32_t root_bit = 1u << root;
       st[0] = {t.dom_size[kr] > 1, C_NONE, 0, C_S1, is_root ? dpeers : 0u};
       st[1] = {any_cross || t.dom_size[kr] > 1, C_S1, (in_root_dom && !is_root) ? root_bit : 0u, C_S2, in_root_dom ? bcross : 0u};
-      st[2] = {true, C_S2, in_root_dom ? 0u : bcross, C_S3, dpeers & ~root_bit};
-      st[3] = {any_intra, C_S3, is_root ? 0u : dpeers, C_NONE, 0};
+      st[2] = {true, C_S2, in_root_dom ? 0u : bcross, C_S3, is_root ? 0u : (dpeers & ~root_bit)};
+      st[3] = {any_intra, C_S3, is_root ? 0u : (dpeers & ~root_bit), C_NONE, 0};
       return 4;
     }
     case OP_REDUCE: {
@@ -390,25 +410,34 @@ void plan_bytes(const Topo& t, int op, int rank, int root, size_t count, int es,
       S += len * (size_t)(n - 1);
       R += len * (size_t)(n - 1);
     } else if (op == OP_BROADCAST) {
-      const int kr = t.rank_dom[root], spj = L / d;
-      if (rank == root)
+      const int kr = t.rank_dom[root], spj = L / d, relay = bcast_relay(t, root), rj = t.rank_idx[root];
+      const bool in_root_dom = (k == kr), is_root = (rank == root);
+      // A: the root scatters every region of its domain (its own to the relay)
+      if (is_root)
         for (int i = 0; i < d; i++)
-          if (i != j) S += region(k, i);  // B1
-      if (k == kr && rank != root) R += region(k, j);
+          if (i != j) S += region(k, i) + (t.members[t.dom_first[k] + i] == relay ? region(k, j) : 0);
+      if (in_root_dom && !is_root) R += region(k, j) + (rank == relay ? region(k, rj) : 0);
+      // B: each root-domain segment crosses once to every other domain (the root's segments via the relay)
       if (D > 1) {
-        for (int s = j * spj; s < (j + 1) * spj; s++) {
-          size_t sl = seg(s + 1) - seg(s);
-          if (k == kr)
-            S += sl * (size_t)(D - 1);  // B2 out: each other domain gets segment s once
-          else
-            R += sl;
+        const bool pushes = in_root_dom && (!is_root || relay < 0);
+        for (int s = 0; s < L; s++) {
+          const size_t sl = seg(s + 1) - seg(s);
+          const int o = owner_of(t, kr, s);
+          const int sender = (o == root && relay >= 0) ? relay : o;
+          if (pushes && sender == rank) S += sl * (size_t)(D - 1);
+          if (!in_root_dom && owner_of(t, k, s) == rank) R += sl;
         }
       }
-      for (int i = 0; i < d; i++)
-        if (i != j) {  // B3: my region to peers (not to the root), peers' regions to me (not if root)
-          int peer = t.members[t.dom_first[k] + i];
-          if (peer != root) S += region(k, j);
-          if (rank != root) R += region(k, i);
+      // C: intra all-gather among the non-root members (the relay also forwards the root's region)
+      if (!is_root)
+        for (int i = 0; i < d; i++) {
+          if (i == j) continue;
+          const int peer = t.members[t.dom_first[k] + i];
+          if (peer == root) continue;
+          S += region(k, j);
+          if (in_root_dom && rank == relay) S += region(k, rj);  // the root's region, on the root's behalf
+          R += region(k, i);
+          if (in_root_dom && peer == relay) R += region(k, rj);
         }
     }
   }
