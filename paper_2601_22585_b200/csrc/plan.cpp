@@ -148,6 +148,16 @@ Geometry make_geometry(const Topo& t, int op, size_t count, int es, int nch_max,
   if (per_ch < tile) tile = std::min(tile, std::max(floor_el, ceil_div(per_ch, q) * q));
   per_ch = ceil_div(count, (size_t)nch_max);
   if (per_ch < tile) tile = std::max(q, ceil_div(per_ch, q) * q);
+  // balance: shrink the tile so every channel gets the same number of tiles (k), instead of some channels
+  // running one extra tile while the others idle (HETCCL_BALANCE=0 keeps the target tile)
+  const char* e3 = getenv("HETCCL_BALANCE");
+  if (!(e3 && *e3 == '0')) {
+    const size_t nt = ceil_div(count, tile);
+    if (nt > (size_t)nch_max) {
+      const size_t k = ceil_div(nt, (size_t)nch_max);
+      tile = std::max(q, ceil_div(ceil_div(count, (size_t)nch_max * k), q) * q);
+    }
+  }
   g.tile = tile;
   g.ntiles = ceil_div(count, tile);
   g.nch = (int)std::min<size_t>((size_t)nch_max, g.ntiles);

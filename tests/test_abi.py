@@ -84,8 +84,14 @@ SPLITS = {"1+1": [0, 1], "2+2": [0, 0, 1, 1], "1+3": [0, 1, 1, 1], "1+1+2": [0, 
           "4+4": [0] * 4 + [1] * 4, "2+6": [0, 0] + [1] * 6, "2+2+4": [0, 0, 1, 1, 2, 2, 2, 2], "8": [0] * 8}
 
 
+@pytest.fixture
+def unbalanced(monkeypatch):
+    """Whole-tile closed forms: keep the target tile (HETCCL_BALANCE=0) so count = k * tile stays whole."""
+    monkeypatch.setenv("HETCCL_BALANCE", "0")
+
+
 @pytest.mark.parametrize("name", sorted(SPLITS))
-def test_allreduce_bytes_closed_form(hc, name):
+def test_allreduce_bytes_closed_form(hc, name, unbalanced):
     """Per-rank AR bytes = S*(2(d-1)/d + 2(D-1)/(D d)) for a count divisible by everything."""
     m = SPLITS[name]
     n, D = len(m), max(m) + 1
@@ -107,7 +113,7 @@ def test_allreduce_bytes_closed_form(hc, name):
 
 
 @pytest.mark.parametrize("name", ["2+6", "4+4", "1+3", "2+2+4"])
-def test_rs_ag_bytes_closed_form(hc, name):
+def test_rs_ag_bytes_closed_form(hc, name, unbalanced):
     """RS received per rank = (d-1)/d*S + (D-1)*S/n; AG is the mirror (sent = that); SURVEY §8(d)."""
     m = SPLITS[name]
     n, D = len(m), max(m) + 1
@@ -124,7 +130,7 @@ def test_rs_ag_bytes_closed_form(hc, name):
         assert ag["bytes_sent"] == recv and ag["bytes_recv"] == sent, (r, ag)
 
 
-def test_rs_2p6_survey_numbers(hc):
+def test_rs_2p6_survey_numbers(hc, unbalanced):
     """C3 (2+6): 2-domain ranks receive 0.625 S, 6-domain ranks 0.958 S."""
     m = SPLITS["2+6"]
     R = 16777216
@@ -147,7 +153,7 @@ def test_conservation(hc):
                 assert s == v, (name, op, count)
 
 
-def test_single_domain_has_no_cross_traffic_and_singletons_no_intra(hc):
+def test_single_domain_has_no_cross_traffic_and_singletons_no_intra(hc, unbalanced):
     """SPEC.md:400 analog: one domain -> only intra bytes (flat 2(n-1)/n S); all-singleton domains ->
     only the cross exchange (2(D-1)/D S)."""
     for m in ([0] * 4, [0, 1, 2, 3]):
@@ -217,7 +223,7 @@ def test_schedule_stage_sets(hc):
 
 
 @pytest.mark.parametrize("name", ["2+2", "1+3", "4+4", "2+6", "2+2+4"])
-def test_reduce_bytes(hc, name):
+def test_reduce_bytes(hc, name, unbalanced):
     """Reduce: the root receives every final piece it does not own ((n-1)/n of S for equal pieces), each
     non-root sends its own final pieces; intra/cross bytes as All-Reduce's reduce-scatter half."""
     m = SPLITS[name]
@@ -239,3 +245,13 @@ def test_all_to_all_bytes(hc):
         n = len(m)
         info = hc.hetccl_plan_info(m, 1, hc.OP_ALL_TO_ALL, 4096, hc.BFLOAT16)
         assert info["bytes_sent"] == info["bytes_recv"] == (n - 1) * 4096 * 2
+
+
+def test_balanced_tiles(hc):
+    """Every channel gets the same number of tiles when the message needs more than one per channel."""
+    for m in ([0, 1], [0, 0, 1, 1], [0, 1, 2, 2]):
+        for mib in (64, 256, 1000):
+            i = hc.hetccl_plan_info(m, 0, hc.OP_ALLREDUCE, mib << 19, hc.BFLOAT16)
+            k = -(-i["ntiles"] // i["nchannels"])
+            assert i["ntiles"] > (k - 1) * i["nchannels"]  # no channel idles for a whole extra tile round
+            assert i["ntiles"] <= k * i["nchannels"]
