@@ -247,8 +247,9 @@ def test_all_to_all_bytes(hc):
         assert info["bytes_sent"] == info["bytes_recv"] == (n - 1) * 4096 * 2
 
 
-def test_balanced_tiles(hc):
-    """Every channel gets the same number of tiles when the message needs more than one per channel."""
+def test_balanced_tiles(hc, monkeypatch):
+    """HETCCL_BALANCE=1: every channel gets the same number of tiles when it needs more than one."""
+    monkeypatch.setenv("HETCCL_BALANCE", "1")
     for m in ([0, 1], [0, 0, 1, 1], [0, 1, 2, 2]):
         for mib in (64, 256, 1000):
             i = hc.hetccl_plan_info(m, 0, hc.OP_ALLREDUCE, mib << 19, hc.BFLOAT16)
