@@ -55,9 +55,12 @@ static size_t ceil_div(size_t a, size_t b) { return (a + b - 1) / b; }
 
 // quantum (elements) a full tile must be a multiple of, so every boundary is V-aligned
 static size_t quantum(const Topo& t, int op, int V) {
-  if (op == OP_ALLREDUCE || op == OP_REDUCE) return (size_t)t.L * t.D * V;
-  if (op == OP_ALL_TO_ALL) return (size_t)V;
-  return (size_t)t.L * V;
+  // HETCCL_ALIGN_B: byte alignment of every piece boundary (default 16 = one vector)
+  const char* e = getenv("HETCCL_ALIGN_B");
+  const size_t mult = std::max<size_t>(1, (e ? (size_t)atol(e) : 16) / 16);
+  if (op == OP_ALLREDUCE || op == OP_REDUCE) return (size_t)t.L * t.D * V * mult;
+  if (op == OP_ALL_TO_ALL) return (size_t)V * mult;
+  return (size_t)t.L * V * mult;
 }
 
 size_t slot_mult_num(const Topo& t, int op, size_t tile) {
