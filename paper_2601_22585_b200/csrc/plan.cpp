@@ -55,9 +55,10 @@ static size_t ceil_div(size_t a, size_t b) { return (a + b - 1) / b; }
 
 // quantum (elements) a full tile must be a multiple of, so every boundary is V-aligned
 static size_t quantum(const Topo& t, int op, int V) {
-  // HETCCL_ALIGN_B: byte alignment of every piece boundary (default 16 = one vector)
+  // HETCCL_ALIGN_B: byte alignment of every piece boundary (default 256: 64-byte aligned pieces of
+  // non-power-of-two tiles cost 7-9%, q20/q21)
   const char* e = getenv("HETCCL_ALIGN_B");
-  const size_t mult = std::max<size_t>(1, (e ? (size_t)atol(e) : 16) / 16);
+  const size_t mult = std::max<size_t>(1, (e ? (size_t)atol(e) : 256) / 16);
   if (op == OP_ALLREDUCE || op == OP_REDUCE) return (size_t)t.L * t.D * V * mult;
   if (op == OP_ALL_TO_ALL) return (size_t)V * mult;
   return (size_t)t.L * V * mult;
@@ -151,10 +152,11 @@ Geometry make_geometry(const Topo& t, int op, size_t count, int es, int nch_max,
   if (per_ch < tile) tile = std::min(tile, std::max(floor_el, ceil_div(per_ch, q) * q));
   per_ch = ceil_div(count, (size_t)nch_max);
   if (per_ch < tile) tile = std::max(q, ceil_div(per_ch, q) * q);
-  // HETCCL_BALANCE=1: shrink the tile so every channel gets the same number of tiles. Measured slower
-  // (q20: 2+2 623 -> 582 GB/s, mux 353 -> 324): the power-of-two tile wins, so it is off by default.
+  // balance: shrink the tile so every channel runs the same number of tiles instead of some channels
+  // running one extra round while the others idle (with 256-byte aligned pieces: 1+1 +5%, 2+2 +1%, mux
+  // neutral, q21/q22; HETCCL_BALANCE=0 keeps the target tile)
   const char* e3 = getenv("HETCCL_BALANCE");
-  if (e3 && *e3 == '1') {
+  if (!(e3 && *e3 == '0')) {
     const size_t nt = ceil_div(count, tile);
     if (nt > (size_t)nch_max) {
       const size_t k = ceil_div(nt, (size_t)nch_max);

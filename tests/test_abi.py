@@ -247,12 +247,17 @@ def test_all_to_all_bytes(hc):
         assert info["bytes_sent"] == info["bytes_recv"] == (n - 1) * 4096 * 2
 
 
-def test_balanced_tiles(hc, monkeypatch):
-    """HETCCL_BALANCE=1: every channel gets the same number of tiles when it needs more than one."""
-    monkeypatch.setenv("HETCCL_BALANCE", "1")
+def test_balanced_tiles(hc):
+    """Every channel gets the same number of tiles when the message needs more than one per channel, and
+    every piece boundary stays 256-byte aligned."""
     for m in ([0, 1], [0, 0, 1, 1], [0, 1, 2, 2]):
         for mib in (64, 256, 1000):
             i = hc.hetccl_plan_info(m, 0, hc.OP_ALLREDUCE, mib << 19, hc.BFLOAT16)
             k = -(-i["ntiles"] // i["nchannels"])
             assert i["ntiles"] > (k - 1) * i["nchannels"]  # no channel idles for a whole extra tile round
             assert i["ntiles"] <= k * i["nchannels"]
+            D = max(m) + 1
+            L = 1
+            for q in range(D):
+                L = L * m.count(q) // __import__("math").gcd(L, m.count(q))
+            assert (i["tile_elems"] * 2) % (256 * L * D) == 0  # bf16 pieces of tile/(L*D) are 256-B multiples
