@@ -279,11 +279,15 @@ hetcclResult_t run_op(hetcclComm_t c, int op, const void* const* sends, void* co
   }
   // direct All-Reduce: stage E has no data, only its S3 wait (my y is complete) -> one end-of-kernel wait
   if (a.direct && env_long("HETCCL_FINAL_WAIT", 1)) a.final_stage = 4;
-  // HETCCL_FLAT_AG=1 (opt-in, direct only): the cross-domain all-gather delivers each final piece to every
+  // flat cross all-gather (direct only): the cross-domain all-gather delivers each final piece to every
   // member of the other domains instead of their segment owner, so the intra-domain forwarding stage D
   // disappears. Same NVLink bytes per rank, more of them cross domains (the paper's hierarchy minimises
-  // those): a deviation for NVSwitch, off by default.
-  if (a.direct && a.final_stage == 4 && c->topo.D > 1 && env_long("HETCCL_FLAT_AG", 0) == 1) {
+  // those): a deviation for NVSwitch (R20). HETCCL_FLAT_AG: 1 always, 0 never, unset = messages of
+  // at most HETCCL_FLAT_AG_MAX_KB (32768) per rank, where one tile per channel walks the stages serially
+  // and dropping one stage pays (q16, 2+2: 8 MiB +19%, 16 MiB +11%, 32 MiB +4%; 64 MiB and up ±0..2%).
+  const long flat_env = env_long("HETCCL_FLAT_AG", -1);
+  const bool flat_band = count * (size_t)es <= (size_t)env_long("HETCCL_FLAT_AG_MAX_KB", 32768) * 1024;
+  if (a.direct && a.final_stage == 4 && c->topo.D > 1 && (flat_env == 1 || (flat_env < 0 && flat_band))) {
     a.flat_ag = 1;
     a.active &= ~(1u << 3);
     for (int r = 0; r < c->n; r++) {

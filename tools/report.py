@@ -34,6 +34,7 @@ def main():
     ap.add_argument("--what", default="ar_sweep")
     ap.add_argument("--out", default=None)
     ap.add_argument("--iters", type=int, default=10)
+    ap.add_argument("--mibs", default="1,2,4,8,16,32,64,128,256,512,1024", help="ar_sweep sizes (MiB per rank)")
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -159,7 +160,7 @@ def main():
     if args.what == "ar_sweep":
         name = DEFAULT[world]
         m = SPLITS[world][name]
-        for mib in [1, 2, 4, 8, 16, 32, 64, 128, 256, 512, 1024]:
+        for mib in [int(v) for v in args.mibs.split(",")]:
             ar_row(name, m, mib)
     elif args.what == "splits":
         for name, m in SPLITS[world].items():
