@@ -116,6 +116,7 @@ struct OpArgs {
                                 //   position; its work must be empty), or -1
   int direct;                   // 1: every rank's recv buffer is addressable here (peer_recv), so All-Reduce
   void* peer_recv[kMaxRanks];   //    writes final pieces straight into them (no staging through scratch)
+  int gpu_scope;                // 1: every rank on this device (rank-multiplexed): flag ops at .gpu scope, else .sys
   int remote_pull;              // 1: pull sources are peers' memory over NVLink (no L2 bulk prefetch of those)
   int flat_ag;                  // 1 (with direct): C writes each final piece into EVERY rank's recv (no stage D)
   int pull;                     // 1 (with direct): every rank's send buffer is addressable (peer_send): the domain

@@ -14,7 +14,8 @@
 //   writer: data stores -> __syncthreads -> fence.acq_rel.sys -> red.relaxed.sys.add(+1) on the
 //           receiver's counter word of this sender;
 //   reader: lane p of warp 0 spins ld.acquire.sys on sender p's word until it reaches the
-//           cumulative target -> __syncthreads -> loads of the data.
+//           cumulative target -> __syncthreads -> loads of the data
+// (.gpu instead of .sys when all ranks share this device: rank-multiplexed comms).
 // Scratch is a ring of nslots slots per channel indexed by the channel's cumulative tile count;
 // before writing a tile's slot a rank waits for the ACK of the tile that last used it. Targets are
 // cumulative across launches (kept in the rank's own base lines), so the protocol needs no host
@@ -39,14 +40,22 @@
 namespace hetccl {
 
 // ------------------------------------------------------------------ PTX primitives -------------
-__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+// Flag operations at system scope (peers are other GPUs, over NVLink) or — when every rank of the
+// communicator runs on this device (rank-multiplexed comms, OpArgs::gpu_scope) — at GPU scope, where the
+// release fence only has to order this SM's stores at L2 instead of across the fabric.
+__device__ __forceinline__ uint64_t ld_acquire(const uint64_t* p, int gpu) {
   uint64_t v;
-  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  if (gpu) asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  else asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
-__device__ __forceinline__ void red_add_relaxed_sys(uint64_t* p, uint64_t v) {
-  asm volatile("red.relaxed.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+__device__ __forceinline__ void fence_acq_rel(int gpu) {
+  if (gpu) asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  else asm volatile("fence.acq_rel.sys;" ::: "memory");
+}
+__device__ __forceinline__ void red_add_relaxed(uint64_t* p, uint64_t v, int gpu) {
+  if (gpu) asm volatile("red.relaxed.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+  else asm volatile("red.relaxed.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ uint64_t globaltimer() {
   uint64_t t;
@@ -607,10 +616,10 @@ struct Pipe {
       for (int q = 0; q < 2 && ok; q++) {
         const uint64_t* w = q ? w2 : w1;
         const uint64_t tg = q ? t2 : t1;
-        if (!w || ld_acquire_sys(w) >= tg) continue;
+        if (!w || ld_acquire(w, a.gpu_scope) >= tg) continue;
         const uint64_t t0 = globaltimer();
         uint32_t spins = 0;
-        while (ld_acquire_sys(w) < tg) {
+        while (ld_acquire(w, a.gpu_scope) < tg) {
           if ((++spins & 1023u) == 0 && (long long)(globaltimer() - t0) > a.timeout_ns) {
             atomicOr(a.err, 1ull + ((unsigned long long)(q ? wc : C_ACK) << 8) + ((unsigned long long)snd << 16));
             ok = false;
@@ -632,10 +641,10 @@ struct Pipe {
       if (!tile_at(it, p, tl)) continue;
       const int s = stage_at[p];
       if (rp.sig_ctr[s] != C_NONE && ((rp.sig_mask[s] >> lane) & 1u))
-        red_add_relaxed_sys(chan_flags(a, lane, ch) + rp.sig_ctr[s] * kLineWords + me, 1);
+        red_add_relaxed(chan_flags(a, lane, ch) + rp.sig_ctr[s] * kLineWords + me, 1, a.gpu_scope);
     }
     long long tl;
-    if (last >= 0 && tile_at(it, last, tl)) red_add_relaxed_sys(chan_flags(a, lane, ch) + C_ACK * kLineWords + me, 1);
+    if (last >= 0 && tile_at(it, last, tl)) red_add_relaxed(chan_flags(a, lane, ch) + C_ACK * kLineWords + me, 1, a.gpu_scope);
   }
   unsigned long long* trc = nullptr;  // per-iteration stamps (HETCCL_TRACE_ITERS), thread 0 only
   __device__ void work(long long it) {
@@ -687,14 +696,14 @@ __device__ __forceinline__ void run_pipeline(const OpArgs& a, Op& op, int me, in
       const Topo& tp = a.topo;
       const int k = tp.rank_dom[me];
       const bool dpeer = P.lane < P.n && P.lane != me && tp.rank_dom[P.lane] == k;
-      fence_acq_rel_sys();
-      if (dpeer) red_add_relaxed_sys(chan_flags(a, P.lane, ch) + C_S1 * kLineWords + me, 1);
+      fence_acq_rel(a.gpu_scope);
+      if (dpeer) red_add_relaxed(chan_flags(a, P.lane, ch) + C_S1 * kLineWords + me, 1, a.gpu_scope);
       if (dpeer) {
         const uint64_t* w = P.F + C_S1 * kLineWords + P.lane;
         const uint64_t tg = ps.base[C_S1][P.lane] + 1;
         const uint64_t t0 = globaltimer();
         uint32_t spins = 0;
-        while (ld_acquire_sys(w) < tg) {
+        while (ld_acquire(w, a.gpu_scope) < tg) {
           if ((++spins & 1023u) == 0 && (long long)(globaltimer() - t0) > a.timeout_ns) {
             atomicOr(a.err, 1ull + ((unsigned long long)C_S1 << 8) + ((unsigned long long)P.lane << 16));
             ps.abort_ = 1;
@@ -723,7 +732,7 @@ __device__ __forceinline__ void run_pipeline(const OpArgs& a, Op& op, int me, in
       stamp(it, 1);
       if (sync_warp) {
         if (it > 0) {
-          fence_acq_rel_sys();
+          fence_acq_rel(a.gpu_scope);
           stamp(it - 1, 3);
           P.signal(it - 1);
         }
@@ -738,7 +747,7 @@ __device__ __forceinline__ void run_pipeline(const OpArgs& a, Op& op, int me, in
       }
     }
     if (sync_warp && nit > 0 && !*(volatile int*)&ps.abort_) {
-      fence_acq_rel_sys();
+      fence_acq_rel(a.gpu_scope);
       stamp(nit - 1, 3);
       P.signal(nit - 1);
     }
@@ -753,7 +762,7 @@ __device__ __forceinline__ void run_pipeline(const OpArgs& a, Op& op, int me, in
       __syncthreads();
       stamp(it, 2);
       if (sync_warp) {
-        fence_acq_rel_sys();
+        fence_acq_rel(a.gpu_scope);
         stamp(it, 3);
         P.signal(it);
       }
@@ -769,7 +778,7 @@ __device__ __forceinline__ void run_pipeline(const OpArgs& a, Op& op, int me, in
       const uint64_t tg = ps.base[wc][P.lane] + P.ntl;
       const uint64_t t0 = globaltimer();
       uint32_t spins = 0;
-      while (ld_acquire_sys(w) < tg) {
+      while (ld_acquire(w, a.gpu_scope) < tg) {
         if ((++spins & 1023u) == 0 && (long long)(globaltimer() - t0) > a.timeout_ns) {
           atomicOr(a.err, 1ull + ((unsigned long long)wc << 8) + ((unsigned long long)P.lane << 16));
           ps.abort_ = 1;
@@ -1429,7 +1438,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_allreduce_oneshot(cons
         const uint64_t* w = F + ctr * kLineWords + lane;
         const uint64_t t0 = globaltimer();
         uint32_t spins = 0;
-        while (ld_acquire_sys(w) < target) {
+        while (ld_acquire(w, a.gpu_scope) < target) {
           if ((++spins & 1023u) == 0 && (long long)(globaltimer() - t0) > a.timeout_ns) {
             atomicOr(a.err, 1ull + ((unsigned long long)ctr << 8) + ((unsigned long long)lane << 16));
             abort_ = 1;
@@ -1443,9 +1452,9 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_allreduce_oneshot(cons
   auto signal_all = [&](int ctr) {
     __syncthreads();
     if (threadIdx.x < 32) {
-      fence_acq_rel_sys();
+      fence_acq_rel(a.gpu_scope);
       const int lane = threadIdx.x;
-      if (lane < n && lane != me) red_add_relaxed_sys(chan_flags(a, lane, ch) + ctr * kLineWords + me, 1);
+      if (lane < n && lane != me) red_add_relaxed(chan_flags(a, lane, ch) + ctr * kLineWords + me, 1, a.gpu_scope);
     }
   };
   // 1. the buffer of op g-2 must be consumed everywhere before it is overwritten

@@ -218,6 +218,9 @@ hetcclResult_t run_op(hetcclComm_t c, int op, const void* const* sends, void* co
   OpArgs a;
   memset(&a, 0, sizeof(a));
   a.topo = c->topo;
+  // rank-multiplexed: every rank runs on this device, so the flag protocol needs only GPU scope
+  // (HETCCL_SYS_SCOPE=1 keeps .sys, for A/B)
+  a.gpu_scope = c->kind == KIND_MUX && env_long("HETCCL_SYS_SCOPE", 0) != 1;
   for (int r = 0; r < c->n; r++) {
     a.mem[r].flags = (uint64_t*)c->mapped[r];
     a.mem[r].scratch = c->mapped[r] + kFlagsReserve;
