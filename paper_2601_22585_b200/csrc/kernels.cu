@@ -210,6 +210,26 @@ __device__ __forceinline__ void prefetch_ahead(const void* src, size_t v0, int t
                : "memory");
 }
 
+#ifndef HETCCL_STAGE_SMEM
+#define HETCCL_STAGE_SMEM 1
+#endif
+// Fold sources are staged through shared memory with cp.async (LDGSTS): each data thread issues the
+// 16-byte loads of up to kStageSrc sources x kUnroll vectors at once and waits once, so a fold keeps
+// kStageSrc times the bytes in flight that register loads (one source at a time) could, without the
+// registers. Each thread reads back only the slots it filled itself (no CTA barrier).
+constexpr int kStageSrc = 5;
+constexpr int kStageVecs = kStageSrc * kUnroll;  // 16-byte slots per data thread
+#if HETCCL_STAGE_SMEM
+__shared__ __align__(16) uint4 g_stage[kStageVecs * kThreads];
+#endif
+__device__ __forceinline__ void cp_async16(uint4* sdst, const void* gsrc) {
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+
 // dst[d][i] = src[i] for every destination d, i < n elements of size ES (bit copy)
 template <int ES>
 __device__ __noinline__ void cta_copy(const void* src, const PtrList& dsts, size_t n) {
@@ -269,6 +289,34 @@ __device__ __noinline__ void cta_fold(const PtrList& srcs, const PtrList& dsts, 
   }
   const int tid = (int)threadIdx.x - g_dbase, nth = g_dnth;
   const size_t nv = all_aligned16(srcs, dsts) ? n / V : 0;
+#if HETCCL_STAGE_SMEM
+  for (size_t v0 = tid; v0 < nv; v0 += (size_t)kUnroll * nth) {
+    for (int s = 0; s < srcs.n; s++) prefetch_ahead(srcs.p[s], v0, tid, (size_t)kUnroll * nth, nv);
+    A acc[kUnroll][V];
+    for (int s0 = 0; s0 < srcs.n; s0 += kStageSrc) {
+      const int g = min(kStageSrc, srcs.n - s0);
+      for (int j = 0; j < g; j++) {
+        const char* sp = (const char*)srcs.p[s0 + j];
+#pragma unroll
+        for (int u = 0; u < kUnroll; u++) {
+          const size_t v = v0 + (size_t)u * nth;
+          if (v < nv) cp_async16(&g_stage[(j * kUnroll + u) * nth + tid], sp + v * 16);
+        }
+      }
+      cp_async_wait_all();
+      for (int j = 0; j < g; j++) {
+#pragma unroll
+        for (int u = 0; u < kUnroll; u++) {
+          const uint4 w = g_stage[(j * kUnroll + u) * nth + tid];
+#pragma unroll
+          for (int e = 0; e < V; e++) {
+            const A x = TR::widen(Vec<S>::get(w, e));
+            acc[u][e] = s0 + j == 0 ? x : comb<OP>(acc[u][e], x);
+          }
+        }
+      }
+    }
+#else
   for (size_t v0 = tid; v0 < nv; v0 += (size_t)kUnroll * nth) {
     for (int s = 0; s < srcs.n; s++) prefetch_ahead(srcs.p[s], v0, tid, (size_t)kUnroll * nth, nv);
     A acc[kUnroll][V];
@@ -298,6 +346,7 @@ __device__ __noinline__ void cta_fold(const PtrList& srcs, const PtrList& dsts, 
 #pragma unroll
         for (int e = 0; e < V; e++) acc[u][e] = comb<OP>(acc[u][e], TR::widen(Vec<S>::get(w[u], e)));
     }
+#endif
     uint4 o[kUnroll];
 #pragma unroll
     for (int u = 0; u < kUnroll; u++)
@@ -348,6 +397,77 @@ __device__ __noinline__ void cta_fold_hier(const PtrList& inner, int kpos, const
   for (int q = 0; q < D; q++)
     if (q != kpos) al |= (uintptr_t)outer.p[q];
   const size_t nv = (all_aligned16(inner, dsts) && (al & 15) == 0) ? n / V : 0;
+#if HETCCL_STAGE_SMEM
+  // operand list in load order: inner[0..inner.n), then outer[q] for q != kpos ascending; staged in groups
+  // of kStageSrc (at 4+4 all five operands of a tile batch are in flight at once)
+  const int L = inner.n + D - 1;
+  auto operand = [&](int j) -> const char* {
+    if (j < inner.n) return (const char*)inner.p[j];
+    const int q = j - inner.n;
+    return (const char*)outer.p[q < kpos ? q : q + 1];
+  };
+  for (size_t v0 = tid; v0 < nv; v0 += (size_t)kUnroll * nth) {
+    for (int s = 0; s < inner.n; s++) prefetch_ahead(inner.p[s], v0, tid, (size_t)kUnroll * nth, nv);
+    for (int q = 0; q < D; q++)
+      if (q != kpos) prefetch_ahead(outer.p[q], v0, tid, (size_t)kUnroll * nth, nv);
+    int lo = 0, hi = 0;  // operands [lo, hi) are in the staging slots [0, hi - lo)
+    auto stage = [&](int j) -> int {
+      if (j >= hi) {
+        lo = j;
+        hi = min(L, j + kStageSrc);
+        for (int k = lo; k < hi; k++) {
+          const char* sp = operand(k);
+#pragma unroll
+          for (int u = 0; u < kUnroll; u++) {
+            const size_t v = v0 + (size_t)u * nth;
+            if (v < nv) cp_async16(&g_stage[((k - lo) * kUnroll + u) * nth + tid], sp + v * 16);
+          }
+        }
+        cp_async_wait_all();
+      }
+      return j - lo;
+    };
+    A acc[kUnroll][V];
+    uint4 pk[kUnroll];
+    for (int s = 0; s < inner.n; s++) {  // ---- inner fold -> P_kpos (narrowed, kept packed) ----
+      const int sl = stage(s);
+#pragma unroll
+      for (int u = 0; u < kUnroll; u++) {
+        const uint4 w = g_stage[(sl * kUnroll + u) * nth + tid];
+#pragma unroll
+        for (int e = 0; e < V; e++) {
+          const A x = TR::widen(Vec<S>::get(w, e));
+          acc[u][e] = s == 0 ? x : comb<OP>(acc[u][e], x);
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; u++)
+#pragma unroll
+      for (int e = 0; e < V; e++) Vec<S>::set(pk[u], e, TR::narrow(acc[u][e]));
+    for (int q = 0; q < D; q++) {  // ---- outer fold over the D domain partials in ascending order ----
+      if (q == kpos) {
+#pragma unroll
+        for (int u = 0; u < kUnroll; u++)
+#pragma unroll
+          for (int e = 0; e < V; e++) {
+            const A x = TR::widen(Vec<S>::get(pk[u], e));
+            acc[u][e] = q == 0 ? x : comb<OP>(acc[u][e], x);
+          }
+        continue;
+      }
+      const int sl = stage(inner.n + (q < kpos ? q : q - 1));
+#pragma unroll
+      for (int u = 0; u < kUnroll; u++) {
+        const uint4 w = g_stage[(sl * kUnroll + u) * nth + tid];
+#pragma unroll
+        for (int e = 0; e < V; e++) {
+          const A x = TR::widen(Vec<S>::get(w, e));
+          acc[u][e] = q == 0 ? x : comb<OP>(acc[u][e], x);
+        }
+      }
+    }
+#else
   for (size_t v0 = tid; v0 < nv; v0 += (size_t)kUnroll * nth) {
     for (int s = 0; s < inner.n; s++) prefetch_ahead(inner.p[s], v0, tid, (size_t)kUnroll * nth, nv);
     for (int q = 0; q < D; q++)
@@ -402,6 +522,7 @@ __device__ __noinline__ void cta_fold_hier(const PtrList& inner, int kpos, const
           acc[u][e] = q == 0 ? x : comb<OP>(acc[u][e], x);
         }
     }
+#endif
     uint4 o[kUnroll];
 #pragma unroll
     for (int u = 0; u < kUnroll; u++)
