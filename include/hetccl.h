@@ -114,6 +114,25 @@ HETCCL_API hetcclResult_t hetccl_comm_destroy(hetcclComm_t comm);
 HETCCL_API hetcclResult_t hetccl_comm_info(hetcclComm_t comm, int* rank, int* nranks, int* domain, int* ndomains,
                                 int* domain_rank, int* domain_size);
 
+/*
+ * NVLS mode (opt-in). With HETCCL_NVLS=1 in the environment of
+ * hetccl_comm_init_all, and every domain of the same size d >= 2 on devices with multicast support,
+ * each domain gets an NVLink SHARP multicast object and hetccl_allreduce (bf16/fp16/fp32 sum, 16-byte
+ * aligned buffers) runs its intra-domain reduce-scatter inside the switch (multimem.ld_reduce, fp32
+ * accumulation) and its intra-domain all-gather as one multicast store (multimem.st); the cross-domain
+ * exchange and fold stay P2P in ascending domain order. The switch's summation order is not R3's, so
+ * results are within the R7 gate but not bitwise those of the oracle (R21). Other dtypes,
+ * ops and unaligned buffers keep the P2P path.
+ *   enabled : 1 if this comm runs All-Reduce in NVLS mode, else 0 (hetccl_get_last_error says why).
+ *   buffer  : this rank's view of its multicast-bound buffer (device memory owned by the comm, valid
+ *             until hetccl_comm_destroy), or NULL. An in-place All-Reduce on it (sendbuf == recvbuf ==
+ *             buffer, count * size a multiple of 16 bytes, at most *bytes) skips the copies in and out.
+ *   bytes   : the buffer's usable size (the chunk size, HETCCL_NVLS_MB rounded to the multicast
+ *             granularity), or 0.
+ * Any output pointer may be NULL. hetcclInvalidArgument on a null comm.
+ */
+HETCCL_API hetcclResult_t hetccl_comm_nvls(hetcclComm_t comm, int* enabled, void** buffer, size_t* bytes);
+
 /* hetcclInternalError if a device-side timeout was recorded on this comm since init (sticky). */
 HETCCL_API hetcclResult_t hetccl_comm_get_async_error(hetcclComm_t comm);
 

@@ -50,6 +50,7 @@ EXPORTED = [
     "hetccl_mux_reduce_scatter", "hetccl_mux_all_gather", "hetccl_mux_broadcast", "hetccl_plan_info",
     "hetccl_plan_stages", "hetccl_comm_get_trace", "hetccl_reduce", "hetccl_all_to_all", "hetccl_mux_reduce",
     "hetccl_mux_all_to_all", "hetccl_mem_alloc", "hetccl_mem_export", "hetccl_mem_connect", "hetccl_mem_free",
+    "hetccl_comm_nvls",
 ]
 
 _lib = None
@@ -95,6 +96,7 @@ def lib():
         "hetccl_mem_export": [vp, vp, vp, ctypes.POINTER(c_size)],
         "hetccl_mem_connect": [vp, vp, vp, c_size],
         "hetccl_mem_free": [vp, vp],
+        "hetccl_comm_nvls": [vp, ip, pp, ctypes.POINTER(c_size)],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -197,6 +199,26 @@ def hetccl_comm_info(comm):
 
 def hetccl_comm_get_async_error(comm):
     _check(lib().hetccl_comm_get_async_error(comm), comm)
+
+
+def hetccl_comm_nvls(comm):
+    """NVLS mode of a hetccl_comm_init_all comm (HETCCL_NVLS=1): (enabled, buffer pointer, usable bytes)."""
+    on, p, nb = ctypes.c_int(0), ctypes.c_void_p(), ctypes.c_size_t(0)
+    _check(lib().hetccl_comm_nvls(comm, ctypes.byref(on), ctypes.byref(p), ctypes.byref(nb)), comm)
+    return bool(on.value), p.value, nb.value
+
+
+def nvls_buffer(comm, numel, dtype, device):
+    """Torch view (on `device`, the comm's GPU) of the first `numel` elements of the comm's multicast-bound
+    buffer: an in-place All-Reduce on it skips the copies in and out of NVLS mode. Owned by the comm."""
+    import torch
+    on, p, nb = hetccl_comm_nvls(comm)
+    es = torch.empty((), dtype=dtype).element_size()
+    if not on or numel * es > nb:
+        raise HetcclError(3, f"NVLS buffer unavailable or too small ({nb} bytes)")
+    name = str(dtype).replace("torch.", "")
+    t = torch.as_tensor(_CudaArray(p, (numel,), _TYPESTR[name] if name != "bfloat16" else "<i2"), device=f"cuda:{device}")
+    return t.view(torch.bfloat16) if dtype == torch.bfloat16 else t
 
 
 def hetccl_comm_get_trace(comm):

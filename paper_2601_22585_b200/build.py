@@ -11,7 +11,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libhetccl.so")
-SOURCES = ["kernels.cu", "runtime.cu", "plan.cpp"]
+SOURCES = ["kernels.cu", "runtime.cu", "plan.cpp", "nvls.cu"]
 HEADERS = ["hetccl_internal.h", os.path.join("..", "..", "include", "hetccl.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",

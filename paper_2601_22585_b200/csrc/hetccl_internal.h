@@ -141,4 +141,13 @@ void make_rank_plan(const Topo& t, int op, int rank, int root, RankPlan* rp);
 void plan_bytes(const Topo& t, int op, int rank, int root, size_t count, int es, size_t tile, size_t* sent,
                 size_t* recv);
 
+// NVLS (nvls.cu, opt-in): multicast-object All-Reduce for single-process multi-GPU communicators
+struct NvlsState;
+int nvls_eligible_topo(const Topo& t);
+int nvls_create(int n, const int* devs, const Topo& t, size_t bytes_per_rank, int nch, NvlsState** out, char* err,
+                size_t errlen);
+void nvls_destroy(NvlsState* s);
+void nvls_buffer(const NvlsState* s, void** p, size_t* bytes);
+int nvls_supports(const NvlsState* s, int dt, int red, const void* send, const void* recv);
+
 }  // namespace hetccl

@@ -1,0 +1,585 @@
+// nvls.cu — opt-in NVLink SHARP (NVLS) All-Reduce for single-process multi-GPU communicators
+// (HETCCL_NVLS=1 at hetccl_comm_init_all).
+//
+// The intra-domain stages of the hierarchy run inside the NVSwitch: every domain (all domains of equal
+// size d >= 2) gets one multicast object; each member binds a buffer of its own HBM to it ("uc", its
+// unicast view) and maps the multicast address ("mc"). Per chunk of CE elements per rank:
+//   1. copy x -> uc (zero-padded to a 16-byte vector), signal N_IN to the domain members;
+//   2. member i waits for N_IN, reads its segment i through mc with multimem.ld_reduce (the switch
+//      sums the d members' copies, fp32 accumulation for bf16/fp16) = this domain's partial P_k,
+//      stores it into its own cross slot and pushes it to member i of every other domain (N_X);
+//   3. waits for the other domains' partials, folds the D partials in ascending domain id in fp32,
+//      narrows once, and multimem.st's the result into every member's uc (one store, the switch
+//      replicates), ACKs the cross slots (N_XACK) and signals N_OUT;
+//   4. after N_OUT from every member, copies uc -> y.
+// When send == recv == the uc buffer itself (hetccl_comm_nvls), steps 1 and 4 are skipped (zero copy).
+// The switch's summation order inside a domain is not reading R3's ascending rank order, so this mode
+// is tolerance-only (R7 gate; R21); the cross-domain fold keeps R3's order.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+
+#include "hetccl_internal.h"
+
+namespace hetccl {
+
+namespace {
+
+constexpr int kNvThreads = 256;
+constexpr int kNvCounters = 4;  // N_IN, N_X, N_XACK, N_OUT
+enum : int { N_IN = 0, N_X = 1, N_XACK = 2, N_OUT = 3 };
+
+// ---------------------------------------------------------------- device -----------------------
+__device__ __forceinline__ uint64_t nv_ld_acquire(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void nv_fence() {
+  asm volatile("fence.proxy.alias;" ::: "memory");  // uc and mc are two virtual aliases of one buffer
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+}
+__device__ __forceinline__ void nv_red(uint64_t* p) {
+  asm volatile("red.relaxed.sys.global.add.u64 [%0], 1;" ::"l"(p) : "memory");
+}
+__device__ __forceinline__ uint4 nv_ld(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.cg.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void nv_st(void* p, const uint4& v) {
+  asm volatile("st.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+
+template <int DT>
+__device__ __forceinline__ uint4 mc_ld_reduce(const void* p);
+template <>
+__device__ __forceinline__ uint4 mc_ld_reduce<DT_BF16>(const void* p) {
+  uint4 v;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.bf16x2 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
+  return v;
+}
+template <>
+__device__ __forceinline__ uint4 mc_ld_reduce<DT_F16>(const void* p) {
+  uint4 v;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.f16x2 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
+  return v;
+}
+template <>
+__device__ __forceinline__ uint4 mc_ld_reduce<DT_F32>(const void* p) {
+  uint4 v;
+  asm volatile("multimem.ld_reduce.relaxed.sys.global.add.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void mc_st(void* p, const uint4& v) {  // bit pattern of 16 bytes
+  asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w) : "memory");
+}
+
+// fp32 views of a 16-byte vector
+template <int DT>
+struct NvVec;
+template <>
+struct NvVec<DT_BF16> {
+  static constexpr int V = 8;
+  __device__ static float get(const uint4& w, int e) {
+    const uint32_t u = (&w.x)[e >> 1];
+    return __uint_as_float((e & 1) ? (u & 0xffff0000u) : (u << 16));
+  }
+  __device__ static void set(uint4& w, int e, float a) {
+    uint32_t& u = (&w.x)[e >> 1];
+    const uint32_t s = __bfloat16_as_ushort(__float2bfloat16_rn(a));
+    u = (e & 1) ? ((u & 0xffffu) | (s << 16)) : ((u & 0xffff0000u) | s);
+  }
+};
+template <>
+struct NvVec<DT_F16> {
+  static constexpr int V = 8;
+  __device__ static float get(const uint4& w, int e) {
+    const uint32_t u = (&w.x)[e >> 1];
+    return __half2float(__ushort_as_half((unsigned short)((e & 1) ? (u >> 16) : (u & 0xffffu))));
+  }
+  __device__ static void set(uint4& w, int e, float a) {
+    uint32_t& u = (&w.x)[e >> 1];
+    const uint32_t s = __half_as_ushort(__float2half_rn(a));
+    u = (e & 1) ? ((u & 0xffffu) | (s << 16)) : ((u & 0xffff0000u) | s);
+  }
+};
+template <>
+struct NvVec<DT_F32> {
+  static constexpr int V = 4;
+  __device__ static float get(const uint4& w, int e) { return __uint_as_float((&w.x)[e]); }
+  __device__ static void set(uint4& w, int e, float a) { (&w.x)[e] = __float_as_uint(a); }
+};
+
+struct NvlsArgs {
+  const char* send;
+  char* recv;
+  size_t count;       // elements per rank
+  size_t ce;          // chunk elements per rank (multiple of d * V)
+  char* uc;           // my unicast view of the domain's multicast buffer
+  char* mc;           // the domain's multicast address (as mapped on my device)
+  char* xs[kMaxRanks];        // cross slots of member i of domain q (q == k: mine)
+  uint64_t* fl[kMaxRanks];    // flag area of every rank
+  size_t xs_slot;     // bytes of one (slot, sender domain) cross buffer = ce / d elements
+  int me, d, D, i, k, nch, zero_copy;
+  int dmem[kMaxRanks];        // ranks of my domain, by index
+  int xrank[kMaxRanks];       // rank of member i of domain q
+  unsigned long long* err;
+  long long timeout_ns;
+};
+
+__device__ __forceinline__ uint64_t* nv_flag(const NvlsArgs& a, int owner, int ch, int ctr, int sender) {
+  return a.fl[owner] + ((size_t)ch * kNvCounters + ctr) * kMaxRanks + sender;
+}
+__device__ __forceinline__ uint64_t* nv_base(const NvlsArgs& a, int ch) {
+  return a.fl[a.me] + (size_t)a.nch * kNvCounters * kMaxRanks + ch;  // a.nch is the comm's fixed channel count
+}
+
+// warp 0: wait until my (ch, ctr) word of every sender in `who` (lane-indexed list of n ranks) reaches tg
+__device__ bool nv_wait(const NvlsArgs& a, int ch, int ctr, const int* who, int n, int skip, uint64_t tg) {
+  const int lane = threadIdx.x & 31;
+  bool ok = true;
+  if (lane < n && lane != skip) {
+    const uint64_t* w = nv_flag(a, a.me, ch, ctr, who[lane]);
+    const uint64_t t0 = [] { uint64_t t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t; }();
+    uint32_t spins = 0;
+    while (nv_ld_acquire(w) < tg) {
+      if ((++spins & 1023u) == 0) {
+        uint64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if ((long long)(t - t0) > a.timeout_ns) {
+          atomicOr(a.err, 1ull + ((unsigned long long)(16 + ctr) << 8) + ((unsigned long long)who[lane] << 16));
+          ok = false;
+          break;
+        }
+      }
+    }
+  }
+  return __all_sync(0xffffffffu, ok);
+}
+// warp 0 (after the CTA's stores and a __syncthreads): release, then +1 on (owner, ch, ctr, me)
+__device__ void nv_signal(const NvlsArgs& a, int ch, int ctr, const int* who, int n, int skip) {
+  const int lane = threadIdx.x & 31;
+  nv_fence();
+  if (lane < n && lane != skip) nv_red(nv_flag(a, who[lane], ch, ctr, a.me));
+}
+
+template <int DT>
+__global__ void __launch_bounds__(kNvThreads) k_nvls_allreduce(NvlsArgs a) {
+  using VV = NvVec<DT>;
+  constexpr int V = VV::V;
+  constexpr int ES = 16 / V;
+  const int ch = blockIdx.x;
+  const int tid = threadIdx.x, nth = blockDim.x;
+  __shared__ int s_abort;
+  __shared__ uint64_t s_base;
+  if (tid == 0) {
+    s_abort = 0;
+    s_base = *nv_base(a, ch);
+  }
+  __syncthreads();
+  const uint64_t base = s_base;
+  const size_t nchunks = (a.count + a.ce - 1) / a.ce;
+  for (size_t g = 0; g < nchunks; ++g) {
+    const uint64_t G = base + g;
+    const size_t c0 = g * a.ce;                                 // first element of the chunk
+    const size_t len = min(a.ce, a.count - c0);
+    const size_t nvec = (len + V - 1) / V;                      // vectors in the (padded) chunk
+    const size_t seg = (nvec + a.d - 1) / a.d;                  // vectors per segment
+    const size_t sub = (seg + a.nch - 1) / a.nch;               // vectors per channel per segment
+    auto range = [&](int s, size_t& lo, size_t& hi) {
+      const size_t s0 = (size_t)s * seg;
+      lo = min(nvec, s0 + min(seg, (size_t)ch * sub));
+      hi = min(nvec, s0 + min(seg, (size_t)(ch + 1) * sub));
+    };
+    // ---- 1. x -> uc (every segment's channel range), zero padding past len ----
+    if (!a.zero_copy) {
+      for (int s = 0; s < a.d; s++) {
+        size_t lo, hi;
+        range(s, lo, hi);
+        for (size_t v = lo + tid; v < hi; v += nth) {
+          uint4 w;
+          if ((v + 1) * V <= len) {
+            w = nv_ld(a.send + (c0 + v * V) * ES);
+          } else {
+            w = make_uint4(0, 0, 0, 0);
+            for (int e = 0; e < V && v * V + e < len; e++) {
+              if (ES == 4) (&w.x)[e] = *(const uint32_t*)(a.send + (c0 + v * V + e) * 4);
+              else reinterpret_cast<uint16_t*>(&w)[e] = *(const uint16_t*)(a.send + (c0 + v * V + e) * 2);
+            }
+          }
+          nv_st(a.uc + v * 16, w);
+        }
+      }
+    }
+    __syncthreads();
+    if (tid < 32) {
+      nv_signal(a, ch, N_IN, a.dmem, a.d, a.i);
+      if (!nv_wait(a, ch, N_IN, a.dmem, a.d, a.i, G + 1)) s_abort = 1;
+      if (a.D > 1 && G >= 2 && !nv_wait(a, ch, N_XACK, a.xrank, a.D, a.k, G - 1)) s_abort = 1;
+      asm volatile("fence.proxy.alias;" ::: "memory");
+    }
+    __syncthreads();
+    if (s_abort) break;
+    size_t lo, hi;
+    range(a.i, lo, hi);
+    const size_t so = (size_t)(G & 1) * a.D;  // slot base (in units of xs_slot) of this chunk
+    // ---- 2. domain partial through the switch -> my cross slot + member i of every other domain ----
+    for (size_t v = lo + tid; v < hi; v += nth) {
+      const uint4 p = mc_ld_reduce<DT>(a.mc + v * 16);
+      const size_t off = (v - (size_t)a.i * seg) * 16;
+      for (int q = 0; q < a.D; q++) nv_st(a.xs[q] + (so + a.k) * a.xs_slot + off, p);
+    }
+    __syncthreads();
+    if (tid < 32) {
+      if (a.D > 1) {
+        nv_signal(a, ch, N_X, a.xrank, a.D, a.k);
+        if (!nv_wait(a, ch, N_X, a.xrank, a.D, a.k, G + 1)) s_abort = 1;
+      }
+    }
+    __syncthreads();
+    if (s_abort) break;
+    // ---- 3. fold the D partials in ascending domain id, narrow once, multicast store ----
+    char* mine = a.xs[a.k] + so * a.xs_slot;
+    for (size_t v = lo + tid; v < hi; v += nth) {
+      const size_t off = (v - (size_t)a.i * seg) * 16;
+      uint4 w = nv_ld(mine + off);
+      if (a.D > 1) {
+        float acc[V];
+#pragma unroll
+        for (int e = 0; e < V; e++) acc[e] = VV::get(w, e);
+        for (int q = 1; q < a.D; q++) {
+          const uint4 u = nv_ld(mine + (size_t)q * a.xs_slot + off);
+#pragma unroll
+          for (int e = 0; e < V; e++) acc[e] = __fadd_rn(acc[e], VV::get(u, e));
+        }
+#pragma unroll
+        for (int e = 0; e < V; e++) VV::set(w, e, acc[e]);
+      }
+      mc_st(a.mc + v * 16, w);
+    }
+    __syncthreads();
+    if (tid < 32) {
+      if (a.D > 1) nv_signal(a, ch, N_XACK, a.xrank, a.D, a.k);
+      nv_signal(a, ch, N_OUT, a.dmem, a.d, a.i);
+      if (!nv_wait(a, ch, N_OUT, a.dmem, a.d, a.i, G + 1)) s_abort = 1;
+      asm volatile("fence.proxy.alias;" ::: "memory");
+    }
+    __syncthreads();
+    if (s_abort) break;
+    // ---- 4. uc -> y ----
+    if (!a.zero_copy) {
+      for (int s = 0; s < a.d; s++) {
+        size_t l2, h2;
+        range(s, l2, h2);
+        for (size_t v = l2 + tid; v < h2; v += nth) {
+          const uint4 w = nv_ld(a.uc + v * 16);
+          if ((v + 1) * V <= len) {
+            nv_st(a.recv + (c0 + v * V) * ES, w);
+          } else {
+            for (int e = 0; e < V && v * V + e < len; e++) {
+              if (ES == 4) *(uint32_t*)(a.recv + (c0 + v * V + e) * 4) = (&w.x)[e];
+              else *(uint16_t*)(a.recv + (c0 + v * V + e) * 2) = reinterpret_cast<const uint16_t*>(&w)[e];
+            }
+          }
+        }
+      }
+      __syncthreads();  // the next chunk's copy-in overwrites uc
+    }
+  }
+  if (tid == 0 && !s_abort) *nv_base(a, ch) = base + nchunks;
+}
+
+// ---------------------------------------------------------------- host: driver entry points -------
+#define NV_FN(name) decltype(&::name) p_##name = nullptr
+struct Drv {
+  NV_FN(cuDeviceGet);
+  NV_FN(cuDeviceGetAttribute);
+  NV_FN(cuMulticastCreate);
+  NV_FN(cuMulticastAddDevice);
+  NV_FN(cuMulticastBindMem);
+  NV_FN(cuMulticastUnbind);
+  NV_FN(cuMulticastGetGranularity);
+  NV_FN(cuMemCreate);
+  NV_FN(cuMemRelease);
+  NV_FN(cuMemAddressReserve);
+  NV_FN(cuMemAddressFree);
+  NV_FN(cuMemMap);
+  NV_FN(cuMemUnmap);
+  NV_FN(cuMemSetAccess);
+  NV_FN(cuMemGetAllocationGranularity);
+  bool ok = false;
+};
+#undef NV_FN
+
+Drv& drv() {
+  static Drv d;
+  static bool tried = false;
+  if (tried) return d;
+  tried = true;
+  bool ok = true;
+  auto get = [&](const char* sym, void** fn) {
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint(sym, fn, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess || !*fn)
+      ok = false;
+  };
+#define NV_GET(name) get(#name, (void**)&d.p_##name)
+  NV_GET(cuDeviceGet);
+  NV_GET(cuDeviceGetAttribute);
+  NV_GET(cuMulticastCreate);
+  NV_GET(cuMulticastAddDevice);
+  NV_GET(cuMulticastBindMem);
+  NV_GET(cuMulticastUnbind);
+  NV_GET(cuMulticastGetGranularity);
+  NV_GET(cuMemCreate);
+  NV_GET(cuMemRelease);
+  NV_GET(cuMemAddressReserve);
+  NV_GET(cuMemAddressFree);
+  NV_GET(cuMemMap);
+  NV_GET(cuMemUnmap);
+  NV_GET(cuMemSetAccess);
+  NV_GET(cuMemGetAllocationGranularity);
+#undef NV_GET
+  d.ok = ok;
+  return d;
+}
+
+struct McShared {  // one multicast object per domain, released with its last member
+  CUmemGenericAllocationHandle h = 0;
+  size_t bytes = 0;
+  int refs = 0;
+};
+
+}  // namespace
+
+struct NvlsState {
+  int dev = 0, rank = 0, nch = 0;
+  size_t bytes = 0;          // uc / mc bytes
+  size_t ce_bytes = 0;       // chunk bytes per rank (multiple of 16 * d)
+  CUmemGenericAllocationHandle uc_h = 0;
+  CUdeviceptr uc = 0, mc = 0;
+  McShared* mcs = nullptr;
+  char* xs = nullptr;        // cross slots [2][D][ce/d] (cudaMalloc)
+  uint64_t* fl = nullptr;    // flags [nch][4][kMaxRanks] + base[nch] (cudaMalloc, zeroed)
+  NvlsArgs tmpl{};           // peers, topology (pointers filled at create)
+};
+
+static void nv_err(char* err, size_t len, const char* what, int r) {
+  if (err && len) snprintf(err, len, "NVLS: %s failed (%d)", what, r);
+}
+
+int nvls_eligible_topo(const Topo& t) {
+  if (t.n < 2) return 0;
+  const int d = t.dom_size[0];
+  if (d < 2) return 0;
+  for (int k = 1; k < t.D; k++)
+    if (t.dom_size[k] != d) return 0;
+  return 1;
+}
+
+void nvls_destroy(NvlsState* s) {
+  if (!s) return;
+  Drv& D = drv();
+  int prev;
+  cudaGetDevice(&prev);
+  cudaSetDevice(s->dev);
+  cudaDeviceSynchronize();
+  if (s->mc) {
+    D.p_cuMemUnmap(s->mc, s->bytes);
+    D.p_cuMemAddressFree(s->mc, s->bytes);
+  }
+  if (s->uc) {
+    D.p_cuMemUnmap(s->uc, s->bytes);
+    D.p_cuMemAddressFree(s->uc, s->bytes);
+  }
+  if (s->mcs && s->mcs->h) {
+    CUdevice cd;
+    if (D.p_cuDeviceGet(&cd, s->dev) == CUDA_SUCCESS) D.p_cuMulticastUnbind(s->mcs->h, cd, 0, s->bytes);
+  }
+  if (s->uc_h) D.p_cuMemRelease(s->uc_h);
+  if (s->mcs && --s->mcs->refs == 0) {
+    if (s->mcs->h) D.p_cuMemRelease(s->mcs->h);
+    delete s->mcs;
+  }
+  if (s->xs) cudaFree(s->xs);
+  if (s->fl) cudaFree(s->fl);
+  cudaSetDevice(prev);
+  delete s;
+}
+
+// every rank of a single-process communicator (devs[r] = device of rank r); out[r] = its state
+int nvls_create(int n, const int* devs, const Topo& t, size_t bytes_per_rank, int nch, NvlsState** out, char* err,
+                size_t errlen) {
+  for (int r = 0; r < n; r++) out[r] = nullptr;
+  if (!nvls_eligible_topo(t)) {
+    nv_err(err, errlen, "domain sizes must be equal and >= 2", 0);
+    return 1;
+  }
+  Drv& D = drv();
+  if (!D.ok) {
+    nv_err(err, errlen, "driver entry points", 0);
+    return 1;
+  }
+  int prev;
+  cudaGetDevice(&prev);
+  const int d = t.dom_size[0];
+  int rc = 0;
+  for (int r = 0; r < n && !rc; r++) {
+    CUdevice cd;
+    int sup = 0;
+    if (D.p_cuDeviceGet(&cd, devs[r]) != CUDA_SUCCESS ||
+        D.p_cuDeviceGetAttribute(&sup, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, cd) != CUDA_SUCCESS || !sup) {
+      nv_err(err, errlen, "multicast not supported on this device", devs[r]);
+      rc = 1;
+    }
+  }
+  if (rc) return rc;
+  // sizes: a multiple of the multicast and allocation granularities; chunk = bytes (16 * d aligned)
+  CUmulticastObjectProp mp{};
+  mp.numDevices = (unsigned)d;
+  mp.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  mp.size = bytes_per_rank;
+  size_t mg = 0, ag = 0;
+  CUmemAllocationProp ap{};
+  ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  ap.location.id = devs[0];
+  ap.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  if ((rc = D.p_cuMulticastGetGranularity(&mg, &mp, CU_MULTICAST_GRANULARITY_MINIMUM)) ||
+      (rc = D.p_cuMemGetAllocationGranularity(&ag, &ap, CU_MEM_ALLOC_GRANULARITY_MINIMUM))) {
+    nv_err(err, errlen, "granularity", rc);
+    return 1;
+  }
+  const size_t gran = std::max(mg, ag);
+  const size_t bytes = (std::max(bytes_per_rank, (size_t)1) + gran - 1) / gran * gran;
+  const size_t unit = (size_t)16 * d;
+  const size_t ce_bytes = bytes / unit * unit;
+  const size_t xs_slot = ce_bytes / d;
+  for (int r = 0; r < n; r++) {
+    out[r] = new NvlsState();
+    out[r]->dev = devs[r];
+    out[r]->rank = r;
+    out[r]->nch = nch;
+    out[r]->bytes = bytes;
+    out[r]->ce_bytes = ce_bytes;
+  }
+  auto fail = [&](const char* what, int code) {
+    nv_err(err, errlen, what, code);
+    for (int r = 0; r < n; r++) {
+      nvls_destroy(out[r]);
+      out[r] = nullptr;
+    }
+    cudaSetDevice(prev);
+    return 1;
+  };
+  // one multicast object per domain; add every member's device before binding memory
+  for (int k = 0; k < t.D; k++) {
+    McShared* m = new McShared();
+    m->bytes = bytes;
+    mp.size = bytes;
+    if ((rc = D.p_cuMulticastCreate(&m->h, &mp))) {
+      delete m;
+      return fail("cuMulticastCreate", rc);
+    }
+    for (int j = 0; j < d; j++) {
+      const int r = t.members[t.dom_first[k] + j];
+      out[r]->mcs = m;
+      m->refs++;
+      CUdevice cd;
+      D.p_cuDeviceGet(&cd, devs[r]);
+      if ((rc = D.p_cuMulticastAddDevice(m->h, cd))) return fail("cuMulticastAddDevice", rc);
+    }
+  }
+  for (int r = 0; r < n; r++) {
+    NvlsState* s = out[r];
+    cudaSetDevice(s->dev);
+    cudaFree(0);
+    CUmemAllocationProp p = ap;
+    p.location.id = s->dev;
+    if ((rc = D.p_cuMemCreate(&s->uc_h, bytes, &p, 0))) return fail("cuMemCreate", rc);
+    if ((rc = D.p_cuMulticastBindMem(s->mcs->h, 0, s->uc_h, 0, bytes, 0))) return fail("cuMulticastBindMem", rc);
+    CUmemAccessDesc acc{};
+    acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    acc.location.id = s->dev;
+    acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    if ((rc = D.p_cuMemAddressReserve(&s->uc, bytes, gran, 0, 0))) return fail("cuMemAddressReserve(uc)", rc);
+    if ((rc = D.p_cuMemMap(s->uc, bytes, 0, s->uc_h, 0))) return fail("cuMemMap(uc)", rc);
+    if ((rc = D.p_cuMemSetAccess(s->uc, bytes, &acc, 1))) return fail("cuMemSetAccess(uc)", rc);
+    if ((rc = D.p_cuMemAddressReserve(&s->mc, bytes, gran, 0, 0))) return fail("cuMemAddressReserve(mc)", rc);
+    if ((rc = D.p_cuMemMap(s->mc, bytes, 0, s->mcs->h, 0))) return fail("cuMemMap(mc)", rc);
+    if ((rc = D.p_cuMemSetAccess(s->mc, bytes, &acc, 1))) return fail("cuMemSetAccess(mc)", rc);
+    if (cudaMalloc((void**)&s->xs, 2 * (size_t)t.D * xs_slot) != cudaSuccess) return fail("cudaMalloc(xs)", 0);
+    const size_t flb = ((size_t)nch * kNvCounters * kMaxRanks + nch) * sizeof(uint64_t);
+    if (cudaMalloc((void**)&s->fl, flb) != cudaSuccess || cudaMemset(s->fl, 0, flb) != cudaSuccess)
+      return fail("cudaMalloc(flags)", 0);
+    if (cudaMemset((void*)s->uc, 0, bytes) != cudaSuccess) return fail("cudaMemset(uc)", 0);
+    if (cudaDeviceSynchronize() != cudaSuccess) return fail("cudaDeviceSynchronize", 0);
+  }
+  for (int r = 0; r < n; r++) {
+    NvlsState* s = out[r];
+    NvlsArgs& a = s->tmpl;
+    memset(&a, 0, sizeof(a));
+    a.me = r;
+    a.d = d;
+    a.D = t.D;
+    a.i = t.rank_idx[r];
+    a.k = t.rank_dom[r];
+    a.nch = nch;
+    a.ce = 0;  // per dtype at launch
+    a.xs_slot = xs_slot;
+    a.uc = (char*)s->uc;
+    a.mc = (char*)s->mc;
+    for (int j = 0; j < d; j++) a.dmem[j] = t.members[t.dom_first[a.k] + j];
+    for (int q = 0; q < t.D; q++) {
+      const int x = t.members[t.dom_first[q] + a.i];
+      a.xrank[q] = x;
+      a.xs[q] = out[x]->xs;
+    }
+    for (int p = 0; p < n; p++) a.fl[p] = out[p]->fl;
+  }
+  cudaSetDevice(prev);
+  return 0;
+}
+
+void nvls_buffer(const NvlsState* s, void** p, size_t* bytes) {
+  if (p) *p = s ? (void*)s->uc : nullptr;
+  if (bytes) *bytes = s ? s->ce_bytes : 0;
+}
+
+int nvls_supports(const NvlsState* s, int dt, int red, const void* send, const void* recv) {
+  if (!s || red != RED_SUM || !(dt == DT_BF16 || dt == DT_F16 || dt == DT_F32)) return 0;
+  return (((uintptr_t)send | (uintptr_t)recv) & 15) == 0;
+}
+
+cudaError_t nvls_allreduce(NvlsState* s, const void* send, void* recv, size_t count, int dt,
+                           unsigned long long* err, long long timeout_ns, cudaStream_t st) {
+  NvlsArgs a = s->tmpl;
+  const int es = dtype_size(dt);
+  a.send = (const char*)send;
+  a.recv = (char*)recv;
+  a.count = count;
+  a.ce = s->ce_bytes / es;
+  a.err = err;
+  a.timeout_ns = timeout_ns;
+  a.zero_copy = send == recv && (const char*)send == (const char*)s->uc && count * es <= s->ce_bytes &&
+                (count * es) % 16 == 0;
+  dim3 grid(s->nch), block(kNvThreads);
+  switch (dt) {
+    case DT_BF16: k_nvls_allreduce<DT_BF16><<<grid, block, 0, st>>>(a); break;
+    case DT_F16: k_nvls_allreduce<DT_F16><<<grid, block, 0, st>>>(a); break;
+    default: k_nvls_allreduce<DT_F32><<<grid, block, 0, st>>>(a); break;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace hetccl

@@ -20,6 +20,8 @@ namespace hetccl {
 cudaError_t launch_collective(const OpArgs& a, int nlocal, int dt, int red, bool cooperative, cudaStream_t s);
 cudaError_t launch_copy(const void* src, void* dst, size_t n, int es, cudaStream_t s);
 int max_coresident(int op, int dt, int red);
+cudaError_t nvls_allreduce(NvlsState* s, const void* send, void* recv, size_t count, int dt, unsigned long long* err,
+                           long long timeout_ns, cudaStream_t st);
 }  // namespace hetccl
 
 using namespace hetccl;
@@ -60,6 +62,7 @@ struct hetcclComm {
     bool ipc[kMaxRanks] = {false};
   };
   std::vector<SymBuf> sym;
+  NvlsState* nvls = nullptr;              // HETCCL_NVLS=1 at hetccl_comm_init_all (nvls.cu), else null
   std::string last_error;
 };
 
@@ -212,6 +215,10 @@ hetcclResult_t run_op(hetcclComm_t c, int op, const void* const* sends, void* co
   DevGuard g(c->device);
   if (c->n == 1) {  // a9: recv <- send
     if (recvs[0]) CUDA_TRY(c, launch_copy(sends[0], recvs[0], recv_elems(op, count, 1), es, stream));
+    return hetcclSuccess;
+  }
+  if (op == OP_ALLREDUCE && c->nvls && nvls_supports(c->nvls, dt, red, sends[0], recvs[0])) {
+    CUDA_TRY(c, nvls_allreduce(c->nvls, sends[0], recvs[0], count, dt, c->err, c->timeout_ns, stream));
     return hetcclSuccess;
   }
   const bool oneshot = op == OP_ALLREDUCE && c->os_bytes > 0 && count * (size_t)es <= c->os_bytes;
@@ -504,6 +511,19 @@ hetcclResult_t hetccl_comm_init_all(hetcclComm_t* comms, int ndev, const int* de
       cs[i]->connected = true;
       comms[i] = cs[i];
     }
+    // HETCCL_NVLS=1 (opt-in, NEXT-1): All-Reduce through per-domain multicast objects (nvls.cu). If the
+    // map or the devices do not allow it the comms stay on the P2P path; hetccl_comm_nvls reports which.
+    if (env_long("HETCCL_NVLS", 0) == 1) {
+      NvlsState* st[kMaxRanks] = {nullptr};
+      char why[256] = {0};
+      const size_t mb = (size_t)std::max(1L, env_long("HETCCL_NVLS_MB", 32));
+      const int nch = (int)std::max(1L, std::min(1024L, env_long("HETCCL_NVLS_NCH", 148)));
+      if (nvls_create(ndev, devlist, t, mb << 20, nch, st, why, sizeof(why)) == 0) {
+        for (int i = 0; i < ndev; i++) cs[i]->nvls = st[i];
+      } else {
+        for (int i = 0; i < ndev; i++) cs[i]->last_error = why;
+      }
+    }
   } else {
     for (int i = 0; i < ndev; i++)
       if (cs[i]) {
@@ -558,6 +578,7 @@ hetcclResult_t hetccl_comm_init_mux(hetcclComm_t* comm, int nranks, const int* r
 
 hetcclResult_t hetccl_comm_destroy(hetcclComm_t c) {
   if (!c) return hetcclInvalidArgument;
+  if (c->nvls) nvls_destroy(c->nvls);
   {
     DevGuard g(c->device);
     cudaDeviceSynchronize();
@@ -586,6 +607,13 @@ hetcclResult_t hetccl_comm_info(hetcclComm_t c, int* rank, int* nranks, int* dom
   if (ndomains) *ndomains = c->topo.D;
   if (domain_rank) *domain_rank = c->topo.rank_idx[c->rank];
   if (domain_size) *domain_size = c->topo.dom_size[c->topo.rank_dom[c->rank]];
+  return hetcclSuccess;
+}
+
+hetcclResult_t hetccl_comm_nvls(hetcclComm_t c, int* enabled, void** buffer, size_t* bytes) {
+  if (!c) return hetcclInvalidArgument;
+  if (enabled) *enabled = c->nvls != nullptr;
+  nvls_buffer(c->nvls, buffer, bytes);
   return hetcclSuccess;
 }
 

@@ -75,6 +75,7 @@ def test_null_and_bad_args_without_gpu(hc):
     assert lib.hetccl_mem_connect(None, None, None, 0) == 4
     assert lib.hetccl_comm_destroy(None) == 4
     assert lib.hetccl_comm_get_async_error(None) == 4
+    assert lib.hetccl_comm_nvls(None, None, None, None) == 4
     shape = (ctypes.c_int * 3)()
     assert lib.hetccl_comm_get_trace(None, None, 0, shape) == 4
     assert lib.hetccl_get_last_error(None) == b"null comm"

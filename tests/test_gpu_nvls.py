@@ -1,0 +1,171 @@
+"""NVLS mode (opt-in HETCCL_NVLS=1): All-Reduce whose intra-domain stages run in the
+NVSwitch through per-domain multicast objects (multimem.ld_reduce / multimem.st), single process driving
+2 or 4 B200s. The switch's summation order inside a domain is not reading R3's, so the bar is the R7 gate
+against an fp64 reference (bf16/fp16), an fp32 recursive-summation bound (fp32), every rank bitwise
+identical, and exact results on integer-valued data (any order sums those exactly)."""
+import numpy as np
+import pytest
+
+import oracle
+from harness import MAPS, as_f64, inputs, to_numpy, to_torch
+
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+
+NVLS_MAPS = ["2", "2+2", "4"]
+
+
+def _ngpu():
+    import torch
+    return torch.cuda.device_count()
+
+
+def _sync(n):
+    import torch
+    for i in range(n):
+        torch.cuda.synchronize(i)
+
+
+@pytest.fixture
+def nvls_env(monkeypatch):
+    monkeypatch.setenv("HETCCL_NVLS", "1")
+    monkeypatch.setenv("HETCCL_TIMEOUT_S", "10")
+    monkeypatch.setenv("HETCCL_NVLS_MB", "2")  # small chunks: multi-chunk ops at test sizes
+
+
+def _comms(m):
+    import paper_2601_22585_b200 as hc
+    comms = hc.hetccl_comm_init_all(list(range(len(m))), m)
+    on, ptr, nb = hc.hetccl_comm_nvls(comms[0])
+    if not on:
+        why = hc.lib().hetccl_get_last_error(comms[0])
+        for c in comms:
+            hc.hetccl_comm_destroy(c)
+        pytest.skip(f"NVLS unavailable: {why}")
+    return comms
+
+
+def _check(got_list, xs, dt, what):
+    F = np.stack([as_f64(x, dt) for x in xs])
+    R = F.sum(0)
+    A = np.abs(F).sum(0)
+    n = len(xs)
+    for r, got in enumerate(got_list):
+        assert np.array_equal(got.view(np.uint8), got_list[0].view(np.uint8)), f"{what}: rank {r} differs from rank 0"
+    g = as_f64(got_list[0], dt)
+    if dt == "f32":
+        u = 2.0 ** -24
+        assert np.all(np.abs(g - R) <= 2 * n * u * A + 1e-30), f"{what}: fp32 bound"
+    else:
+        assert np.all(np.abs(g - R) <= 1e-2 * A + 1e-30), f"{what}: elementwise gate"
+        nrm = np.linalg.norm(R)
+        if nrm > 0:
+            assert np.linalg.norm(g - R) / nrm <= 1e-2, f"{what}: normwise gate"
+
+
+@pytest.mark.parametrize("name", NVLS_MAPS)
+@pytest.mark.parametrize("dt", ["bf16", "f16", "f32"])
+@pytest.mark.parametrize("count", [1, 7, 5 * 8192 + 333, (3 << 20) // 2 + 5])
+def test_nvls_allreduce(name, dt, count, nvls_env):
+    import paper_2601_22585_b200 as hc
+    m = MAPS[name]
+    n = len(m)
+    if _ngpu() < n:
+        pytest.skip(f"needs {n} GPUs")
+    comms = _comms(m)
+    try:
+        for it in range(2):
+            xs = inputs("normal", 31 + it, n, count, dt)
+            sends = [to_torch(xs[r], dt, f"cuda:{r}") for r in range(n)]
+            recvs = [s.clone().fill_(0) for s in sends]
+            _sync(n)
+            for r in range(n):
+                hc.allreduce(sends[r], recvs[r], comms[r])
+            _sync(n)
+            for c in comms:
+                hc.hetccl_comm_get_async_error(c)
+            _check([to_numpy(y, dt) for y in recvs], xs, dt, f"{name} {dt} n={count} it={it}")
+    finally:
+        for c in comms:
+            hc.hetccl_comm_destroy(c)
+
+
+@pytest.mark.parametrize("name", NVLS_MAPS)
+def test_nvls_exact_on_integers_and_inplace(name, nvls_env):
+    """Small integers sum exactly in any order: NVLS equals the oracle bitwise; in place too."""
+    import torch
+    import paper_2601_22585_b200 as hc
+    m = MAPS[name]
+    n = len(m)
+    if _ngpu() < n:
+        pytest.skip(f"needs {n} GPUs")
+    count = 3 * 65536 + 11
+    rng = np.random.default_rng(5)
+    xs = [rng.integers(-8, 9, count).astype(np.float32) for _ in range(n)]
+    xs = [np.frombuffer(torch.from_numpy(x).bfloat16().view(torch.int16).numpy().tobytes(), np.uint16) for x in xs]
+    comms = _comms(m)
+    try:
+        bufs = [to_torch(xs[r], "bf16", f"cuda:{r}") for r in range(n)]
+        _sync(n)
+        for r in range(n):
+            hc.allreduce(bufs[r], bufs[r], comms[r])
+        _sync(n)
+        want = oracle.allreduce(xs, m, "bf16", "sum")
+        for r in range(n):
+            assert np.array_equal(to_numpy(bufs[r], "bf16"), want), f"{name} rank {r}"
+    finally:
+        for c in comms:
+            hc.hetccl_comm_destroy(c)
+
+
+@pytest.mark.parametrize("name", ["2", "2+2"])
+def test_nvls_zero_copy_buffer(name, nvls_env):
+    """In place on the comm's multicast-bound buffer: no copies in or out; repeated ops (slot reuse)."""
+    import paper_2601_22585_b200 as hc
+    m = MAPS[name]
+    n = len(m)
+    if _ngpu() < n:
+        pytest.skip(f"needs {n} GPUs")
+    comms = _comms(m)
+    try:
+        count = 65536 * 3
+        for it in range(3):
+            xs = inputs("normal", 40 + it, n, count, "bf16")
+            bufs = [hc.nvls_buffer(comms[r], count, __import__("torch").bfloat16, r) for r in range(n)]
+            for r in range(n):
+                bufs[r].copy_(to_torch(xs[r], "bf16", f"cuda:{r}"))
+            _sync(n)
+            for r in range(n):
+                hc.allreduce(bufs[r], bufs[r], comms[r])
+            _sync(n)
+            _check([to_numpy(b, "bf16") for b in bufs], xs, "bf16", f"{name} zero-copy it={it}")
+    finally:
+        for c in comms:
+            hc.hetccl_comm_destroy(c)
+
+
+def test_nvls_ineligible_map_stays_p2p(monkeypatch):
+    """Unequal domains (1+3) or singleton domains (1+1): NVLS is not set up, All-Reduce stays bit-exact P2P."""
+    import paper_2601_22585_b200 as hc
+    monkeypatch.setenv("HETCCL_NVLS", "1")
+    for name in ("1+1", "1+3"):
+        m = MAPS[name]
+        n = len(m)
+        if _ngpu() < n:
+            continue
+        comms = hc.hetccl_comm_init_all(list(range(n)), m)
+        try:
+            assert hc.hetccl_comm_nvls(comms[0])[0] is False
+            count = 4099
+            xs = inputs("normal", 3, n, count, "bf16")
+            sends = [to_torch(xs[r], "bf16", f"cuda:{r}") for r in range(n)]
+            recvs = [s.clone() for s in sends]
+            _sync(n)
+            for r in range(n):
+                hc.allreduce(sends[r], recvs[r], comms[r])
+            _sync(n)
+            want = oracle.allreduce(xs, m, "bf16", "sum")
+            for r in range(n):
+                assert np.array_equal(to_numpy(recvs[r], "bf16"), want)
+        finally:
+            for c in comms:
+                hc.hetccl_comm_destroy(c)
