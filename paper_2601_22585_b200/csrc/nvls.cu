@@ -222,6 +222,7 @@ __global__ void __launch_bounds__(kNvThreads) k_nvls_allreduce(NvlsArgs a) {
         }
       }
     }
+    nv_fence();  // every thread: its unicast stores are read next through the multicast alias by peers
     __syncthreads();
     if (tid < 32) {
       nv_signal(a, ch, N_IN, a.dmem, a.d, a.i);
@@ -231,6 +232,7 @@ __global__ void __launch_bounds__(kNvThreads) k_nvls_allreduce(NvlsArgs a) {
     }
     __syncthreads();
     if (s_abort) break;
+    asm volatile("fence.proxy.alias;" ::: "memory");
     size_t lo, hi;
     range(a.i, lo, hi);
     const size_t so = (size_t)(G & 1) * a.D;  // slot base (in units of xs_slot) of this chunk
@@ -268,6 +270,7 @@ __global__ void __launch_bounds__(kNvThreads) k_nvls_allreduce(NvlsArgs a) {
       }
       mc_st(a.mc + v * 16, w);
     }
+    nv_fence();  // every thread: its multicast stores are complete before the N_OUT release
     __syncthreads();
     if (tid < 32) {
       if (a.D > 1) nv_signal(a, ch, N_XACK, a.xrank, a.D, a.k);
@@ -277,6 +280,7 @@ __global__ void __launch_bounds__(kNvThreads) k_nvls_allreduce(NvlsArgs a) {
     }
     __syncthreads();
     if (s_abort) break;
+    asm volatile("fence.proxy.alias;" ::: "memory");
     // ---- 4. uc -> y ----
     if (!a.zero_copy) {
       for (int s = 0; s < a.d; s++) {

@@ -50,7 +50,8 @@ def _check(got_list, xs, dt, what):
     A = np.abs(F).sum(0)
     n = len(xs)
     for r, got in enumerate(got_list):
-        assert np.array_equal(got.view(np.uint8), got_list[0].view(np.uint8)), f"{what}: rank {r} differs from rank 0"
+        bad = np.nonzero(got != got_list[0])[0]
+        assert bad.size == 0, f"{what}: rank {r} differs from rank 0 at {bad.size} elements, first {bad[:8].tolist()}"
     g = as_f64(got_list[0], dt)
     if dt == "f32":
         u = 2.0 ** -24
