@@ -195,7 +195,10 @@ __global__ void __launch_bounds__(kNvThreads) k_nvls_allreduce(NvlsArgs a) {
     const size_t c0 = g * a.ce;                                 // first element of the chunk
     const size_t len = min(a.ce, a.count - c0);
     const size_t nvec = (len + V - 1) / V;                      // vectors in the (padded) chunk
-    const size_t seg = (nvec + a.d - 1) / a.d;                  // vectors per segment
+    // the partition is that of a FULL chunk on every chunk (a short last chunk only clips it), so a uc
+    // vector always belongs to the same channel: a channel never writes the next chunk into a range
+    // another channel may still be copying out
+    const size_t seg = a.ce / V / a.d;                          // vectors per segment
     const size_t sub = (seg + a.nch - 1) / a.nch;               // vectors per channel per segment
     auto range = [&](int s, size_t& lo, size_t& hi) {
       const size_t s0 = (size_t)s * seg;
@@ -222,7 +225,6 @@ __global__ void __launch_bounds__(kNvThreads) k_nvls_allreduce(NvlsArgs a) {
         }
       }
     }
-    nv_fence();  // every thread: its unicast stores are read next through the multicast alias by peers
     __syncthreads();
     if (tid < 32) {
       nv_signal(a, ch, N_IN, a.dmem, a.d, a.i);
@@ -232,7 +234,6 @@ __global__ void __launch_bounds__(kNvThreads) k_nvls_allreduce(NvlsArgs a) {
     }
     __syncthreads();
     if (s_abort) break;
-    asm volatile("fence.proxy.alias;" ::: "memory");
     size_t lo, hi;
     range(a.i, lo, hi);
     const size_t so = (size_t)(G & 1) * a.D;  // slot base (in units of xs_slot) of this chunk
@@ -270,7 +271,6 @@ __global__ void __launch_bounds__(kNvThreads) k_nvls_allreduce(NvlsArgs a) {
       }
       mc_st(a.mc + v * 16, w);
     }
-    nv_fence();  // every thread: its multicast stores are complete before the N_OUT release
     __syncthreads();
     if (tid < 32) {
       if (a.D > 1) nv_signal(a, ch, N_XACK, a.xrank, a.D, a.k);
@@ -280,7 +280,6 @@ __global__ void __launch_bounds__(kNvThreads) k_nvls_allreduce(NvlsArgs a) {
     }
     __syncthreads();
     if (s_abort) break;
-    asm volatile("fence.proxy.alias;" ::: "memory");
     // ---- 4. uc -> y ----
     if (!a.zero_copy) {
       for (int s = 0; s < a.d; s++) {
