@@ -224,6 +224,9 @@ __global__ void __launch_bounds__(kNvThreads) k_nvls_allreduce(NvlsArgs a) {
           nv_st(a.uc + v * 16, w);
         }
       }
+      // every storing thread orders its unicast stores before the peers' reads through the multicast
+      // alias (a warp-0 fence after the barrier was not enough: q31, stale inputs in a chunk's reduce)
+      nv_fence();
     }
     __syncthreads();
     if (tid < 32) {

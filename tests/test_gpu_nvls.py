@@ -57,7 +57,8 @@ def _check(got_list, xs, dt, what):
         u = 2.0 ** -24
         assert np.all(np.abs(g - R) <= 2 * n * u * A + 1e-30), f"{what}: fp32 bound"
     else:
-        assert np.all(np.abs(g - R) <= 1e-2 * A + 1e-30), f"{what}: elementwise gate"
+        bad = np.nonzero(np.abs(g - R) > 1e-2 * A + 1e-30)[0]
+        assert bad.size == 0, f"{what}: elementwise gate fails at {bad.size} elements, first {bad[:8].tolist()}"
         nrm = np.linalg.norm(R)
         if nrm > 0:
             assert np.linalg.norm(g - R) / nrm <= 1e-2, f"{what}: normwise gate"
