@@ -195,10 +195,10 @@ __global__ void __launch_bounds__(kNvThreads) k_nvls_allreduce(NvlsArgs a) {
     const size_t c0 = g * a.ce;                                 // first element of the chunk
     const size_t len = min(a.ce, a.count - c0);
     const size_t nvec = (len + V - 1) / V;                      // vectors in the (padded) chunk
-    // the partition is that of a FULL chunk on every chunk (a short last chunk only clips it), so a uc
-    // vector always belongs to the same channel: a channel never writes the next chunk into a range
-    // another channel may still be copying out
-    const size_t seg = a.ce / V / a.d;                          // vectors per segment
+    // every chunk of an op uses the partition of its first chunk (a short last chunk only clips it), so
+    // a uc vector always belongs to the same channel: a channel never writes the next chunk into a range
+    // another channel may still be copying out (q30); ops are ordered by the kernel boundary
+    const size_t seg = ((min(a.ce, a.count) + V - 1) / V + a.d - 1) / a.d;  // vectors per segment
     const size_t sub = (seg + a.nch - 1) / a.nch;               // vectors per channel per segment
     auto range = [&](int s, size_t& lo, size_t& hi) {
       const size_t s0 = (size_t)s * seg;
