@@ -135,10 +135,13 @@ def _op(op):
     return _OPS[op] if isinstance(op, str) else int(op)
 
 
-def _stream(stream):
+def _stream(stream, like=None):
+    """A raw cudaStream_t: `stream` as given, else the current stream of the device `like` (a tensor) lives on
+    (a comm on another GPU than the current one must not be handed the current device's stream)."""
     if stream is None:
         import torch
-        return torch.cuda.current_stream().cuda_stream
+        dev = like.device if like is not None and hasattr(like, "device") else None
+        return torch.cuda.current_stream(dev).cuda_stream
     if isinstance(stream, int):
         return stream
     return stream.cuda_stream
@@ -385,52 +388,52 @@ def hetccl_mux_all_to_all(sendbufs, recvbufs, count, dtype, comm, stream):
 
 # tensor conveniences (same calls; count/dtype taken from the tensors)
 def allreduce(send, recv, comm, op="sum", stream=None):
-    hetccl_allreduce(_ptr(send), _ptr(recv), recv.numel(), dtype_code(recv.dtype), op, comm, _stream(stream))
+    hetccl_allreduce(_ptr(send), _ptr(recv), recv.numel(), dtype_code(recv.dtype), op, comm, _stream(stream, recv))
 
 
 def reduce_scatter(send, recv, comm, op="sum", stream=None):
-    hetccl_reduce_scatter(_ptr(send), _ptr(recv), recv.numel(), dtype_code(recv.dtype), op, comm, _stream(stream))
+    hetccl_reduce_scatter(_ptr(send), _ptr(recv), recv.numel(), dtype_code(recv.dtype), op, comm, _stream(stream, recv))
 
 
 def all_gather(send, recv, comm, stream=None):
-    hetccl_all_gather(_ptr(send), _ptr(recv), send.numel(), dtype_code(send.dtype), comm, _stream(stream))
+    hetccl_all_gather(_ptr(send), _ptr(recv), send.numel(), dtype_code(send.dtype), comm, _stream(stream, send))
 
 
 def broadcast(send, recv, root, comm, stream=None):
-    hetccl_broadcast(_ptr(send), _ptr(recv), recv.numel(), dtype_code(recv.dtype), root, comm, _stream(stream))
+    hetccl_broadcast(_ptr(send), _ptr(recv), recv.numel(), dtype_code(recv.dtype), root, comm, _stream(stream, recv))
 
 
 def reduce(send, recv, root, comm, op="sum", stream=None):
     """recv may be None on non-root ranks."""
-    hetccl_reduce(_ptr(send), _ptr(recv), send.numel(), dtype_code(send.dtype), op, root, comm, _stream(stream))
+    hetccl_reduce(_ptr(send), _ptr(recv), send.numel(), dtype_code(send.dtype), op, root, comm, _stream(stream, send))
 
 
 def all_to_all(send, recv, comm, stream=None):
     """send/recv hold nranks equal blocks."""
     n = hetccl_comm_info(comm)["nranks"]
-    hetccl_all_to_all(_ptr(send), _ptr(recv), send.numel() // n, dtype_code(send.dtype), comm, _stream(stream))
+    hetccl_all_to_all(_ptr(send), _ptr(recv), send.numel() // n, dtype_code(send.dtype), comm, _stream(stream, send))
 
 
 def mux_reduce(sends, recvs, root, comm, op="sum", stream=None):
-    hetccl_mux_reduce(sends, recvs, sends[0].numel(), dtype_code(sends[0].dtype), op, root, comm, _stream(stream))
+    hetccl_mux_reduce(sends, recvs, sends[0].numel(), dtype_code(sends[0].dtype), op, root, comm, _stream(stream, sends[0]))
 
 
 def mux_all_to_all(sends, recvs, comm, stream=None):
     n = len(sends)
-    hetccl_mux_all_to_all(sends, recvs, sends[0].numel() // n, dtype_code(sends[0].dtype), comm, _stream(stream))
+    hetccl_mux_all_to_all(sends, recvs, sends[0].numel() // n, dtype_code(sends[0].dtype), comm, _stream(stream, sends[0]))
 
 
 def mux_allreduce(sends, recvs, comm, op="sum", stream=None):
-    hetccl_mux_allreduce(sends, recvs, recvs[0].numel(), dtype_code(recvs[0].dtype), op, comm, _stream(stream))
+    hetccl_mux_allreduce(sends, recvs, recvs[0].numel(), dtype_code(recvs[0].dtype), op, comm, _stream(stream, sends[0]))
 
 
 def mux_reduce_scatter(sends, recvs, comm, op="sum", stream=None):
-    hetccl_mux_reduce_scatter(sends, recvs, recvs[0].numel(), dtype_code(recvs[0].dtype), op, comm, _stream(stream))
+    hetccl_mux_reduce_scatter(sends, recvs, recvs[0].numel(), dtype_code(recvs[0].dtype), op, comm, _stream(stream, sends[0]))
 
 
 def mux_all_gather(sends, recvs, comm, stream=None):
-    hetccl_mux_all_gather(sends, recvs, sends[0].numel(), dtype_code(sends[0].dtype), comm, _stream(stream))
+    hetccl_mux_all_gather(sends, recvs, sends[0].numel(), dtype_code(sends[0].dtype), comm, _stream(stream, sends[0]))
 
 
 def mux_broadcast(sends, recvs, root, comm, stream=None):
-    hetccl_mux_broadcast(sends, recvs, recvs[0].numel(), dtype_code(recvs[0].dtype), root, comm, _stream(stream))
+    hetccl_mux_broadcast(sends, recvs, recvs[0].numel(), dtype_code(recvs[0].dtype), root, comm, _stream(stream, sends[0]))

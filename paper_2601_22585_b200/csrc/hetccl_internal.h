@@ -110,8 +110,9 @@ struct OpArgs {
   int trace_iters;
   int ws;                       // 0: plain pipeline; k >= 2: warp-specialised, consumers k positions after producers
   int nslots;                   // scratch ring depth (> pipeline positions)
-  size_t os_off;                // one-shot area: byte offset in every rank's scratch, bytes per (buffer, sender)
-  size_t os_stride;
+  size_t os_off;                // one-shot area: byte offset in every rank's scratch, bytes per (buffer, sender),
+  size_t os_stride;             //   bytes per (buffer, sender, channel) — each channel's region is private to it
+  size_t os_chan;
   int final_stage;              // logical stage whose waits become ONE end-of-kernel wait (no pipeline
                                 //   position; its work must be empty), or -1
   int direct;                   // 1: every rank's recv buffer is addressable here (peer_recv), so All-Reduce

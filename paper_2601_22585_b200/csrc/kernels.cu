@@ -1549,8 +1549,9 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_allreduce_oneshot(cons
   const int buf = (int)(g & 1);
   const size_t chunk = (a.count + (size_t)a.nch * V - 1) / ((size_t)a.nch * V) * V;
   const size_t lo = min(a.count, (size_t)ch * chunk), hi = min(a.count, lo + chunk);
+  // channel ch's private region of (owner, buffer, sender): its chunk [lo, hi) lands at offset 0
   auto area = [&](int owner, int sender) -> T* {
-    return (T*)(a.mem[owner].scratch + a.os_off + ((size_t)buf * n + sender) * a.os_stride);
+    return (T*)(a.mem[owner].scratch + a.os_off + ((size_t)buf * n + sender) * a.os_stride + (size_t)ch * a.os_chan);
   };
   auto wait_all = [&](int ctr, uint64_t target) {
     if (threadIdx.x < 32) {
@@ -1585,7 +1586,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_allreduce_oneshot(cons
   {
     PtrList dst;
     for (int r = 0; r < n; r++)
-      if (r != me) dst.add(area(r, me) + lo);
+      if (r != me) dst.add(area(r, me));
     cta_copy<sizeof(T)>(x + lo, dst, hi - lo);
   }
   signal_all(C_OS);
@@ -1594,7 +1595,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_allreduce_oneshot(cons
   if (abort_) return;
   {
     PtrList src, dst;
-    for (int r = 0; r < n; r++) src.add(r == me ? (const void*)(x + lo) : (const void*)(area(me, r) + lo));
+    for (int r = 0; r < n; r++) src.add(r == me ? (const void*)(x + lo) : (const void*)area(me, r));
     dst.add(y + lo);
     cta_fold_domains<T, OP>(src, a.topo, dst, hi - lo);
   }

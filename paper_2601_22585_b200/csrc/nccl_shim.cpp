@@ -17,6 +17,7 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
@@ -87,35 +88,55 @@ bool domain_map(int n, std::vector<int>* m) {
   return hetccl_validate_map(n, m->data(), nullptr) == hetcclSuccess;
 }
 
-// bootstrap a hetccl communicator next to a freshly created NCCL communicator
+// bootstrap a hetccl communicator next to a freshly created NCCL communicator. Every rank takes part in
+// both real collectives below whatever happened locally (a rank that skipped them would leave the others
+// blocked inside NCCL): the blob all-gather (a rank that failed locally sends an all-zero, invalid blob)
+// and an all-reduce(min) of "connected" flags, so either every rank attaches or none does.
 void attach(ncclComm_t comm, int nranks, int rank) {
   const char* off = getenv("HETCCL_SHIM_DISABLE");
   if (off && *off && *off != '0') return;
   std::vector<int> m;
+  // same decision on every rank: nranks and the environment are shared
   if (nranks < 2 || nranks > HETCCL_MAX_RANKS || !domain_map(nranks, &m)) return;
   int dev = 0;
   cudaGetDevice(&dev);
-  hetcclComm_t hc = nullptr;
-  if (hetccl_comm_init(&hc, nranks, rank, m.data(), dev) != hetcclSuccess) return;
-  std::vector<char> blob(HETCCL_BLOB_BYTES), all((size_t)nranks * HETCCL_BLOB_BYTES);
-  size_t nb = blob.size();
+  const size_t all_bytes = (size_t)nranks * HETCCL_BLOB_BYTES;
+  std::vector<char> blob(HETCCL_BLOB_BYTES, 0), all(all_bytes);
   char* d = nullptr;
-  cudaStream_t st = nullptr;
-  bool ok = hetccl_comm_export(hc, blob.data(), &nb) == hetcclSuccess &&
-            cudaMalloc((void**)&d, all.size()) == cudaSuccess && cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) == cudaSuccess &&
-            cudaMemcpy(d + (size_t)rank * HETCCL_BLOB_BYTES, blob.data(), HETCCL_BLOB_BYTES, cudaMemcpyHostToDevice) == cudaSuccess;
-  if (ok) {
-    auto ag = real<ncclResult_t (*)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t)>("ncclAllGather");
-    ok = ag(d + (size_t)rank * HETCCL_BLOB_BYTES, d, HETCCL_BLOB_BYTES, ncclInt8, comm, st) == ncclSuccess &&
-         cudaStreamSynchronize(st) == cudaSuccess &&
-         cudaMemcpy(all.data(), d, all.size(), cudaMemcpyDeviceToHost) == cudaSuccess &&
-         hetccl_comm_connect(hc, all.data(), all.size()) == hetcclSuccess;
+  if (cudaMalloc((void**)&d, all_bytes + 16) != cudaSuccess) {
+    // without a device buffer this rank cannot join the bootstrap collectives: a hang would follow
+    fprintf(stderr, "hetccl shim: rank %d cannot allocate the bootstrap buffer; aborting\n", rank);
+    abort();
   }
-  if (d) cudaFree(d);
+  cudaStream_t st = nullptr;
+  if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) st = nullptr;  // legacy stream
+  hetcclComm_t hc = nullptr;
+  size_t nb = blob.size();
+  bool local_ok = hetccl_comm_init(&hc, nranks, rank, m.data(), dev) == hetcclSuccess &&
+                  hetccl_comm_export(hc, blob.data(), &nb) == hetcclSuccess;
+  if (!local_ok) std::fill(blob.begin(), blob.end(), 0);
+  auto ag = real<ncclResult_t (*)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t)>("ncclAllGather");
+  auto ar = real<ncclResult_t (*)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t)>(
+      "ncclAllReduce");
+  bool coll_ok = cudaMemcpy(d + (size_t)rank * HETCCL_BLOB_BYTES, blob.data(), HETCCL_BLOB_BYTES,
+                            cudaMemcpyHostToDevice) == cudaSuccess;
+  coll_ok = ag(d + (size_t)rank * HETCCL_BLOB_BYTES, d, HETCCL_BLOB_BYTES, ncclInt8, comm, st) == ncclSuccess && coll_ok;
+  coll_ok = cudaStreamSynchronize(st) == cudaSuccess && coll_ok;
+  coll_ok = cudaMemcpy(all.data(), d, all_bytes, cudaMemcpyDeviceToHost) == cudaSuccess && coll_ok;
+  // connect fails (invalid blob) on every rank if any rank failed locally; it can also fail on one rank only
+  // (an IPC open), hence the agreement round
+  int flag = (local_ok && coll_ok && hetccl_comm_connect(hc, all.data(), all_bytes) == hetcclSuccess) ? 1 : 0;
+  int* dflag = (int*)(d + all_bytes);
+  bool agreed = cudaMemcpy(dflag, &flag, sizeof(int), cudaMemcpyHostToDevice) == cudaSuccess;
+  agreed = ar(dflag, dflag, 1, ncclInt32, ncclMin, comm, st) == ncclSuccess && agreed;
+  agreed = cudaStreamSynchronize(st) == cudaSuccess && agreed;
+  int all_ok = 0;
+  agreed = cudaMemcpy(&all_ok, dflag, sizeof(int), cudaMemcpyDeviceToHost) == cudaSuccess && agreed;
+  cudaFree(d);
   if (st) cudaStreamDestroy(st);
-  if (!ok) {
-    if (verbose()) fprintf(stderr, "hetccl shim: rank %d bootstrap failed, using NCCL\n", rank);
-    hetccl_comm_destroy(hc);
+  if (!agreed || all_ok != 1) {
+    if (verbose()) fprintf(stderr, "hetccl shim: rank %d: bootstrap failed on some rank (local %d), using NCCL\n", rank, flag);
+    if (hc) hetccl_comm_destroy(hc);
     return;
   }
   std::lock_guard<std::mutex> l(g_mu);
@@ -129,7 +150,9 @@ hetcclComm_t lookup(ncclComm_t comm) {
   return it == g_map.end() ? nullptr : it->second;
 }
 
-void detach(ncclComm_t comm) {
+// abort = true (ncclCommAbort): forget the hetccl comm without destroying it — destroy synchronises the
+// device, which can block for the whole device timeout when a peer is gone; its memory is leaked instead.
+void detach(ncclComm_t comm, bool abort_ = false) {
   hetcclComm_t hc = nullptr;
   {
     std::lock_guard<std::mutex> l(g_mu);
@@ -137,6 +160,10 @@ void detach(ncclComm_t comm) {
     if (it == g_map.end()) return;
     hc = it->second;
     g_map.erase(it);
+  }
+  if (abort_) {
+    if (verbose()) fprintf(stderr, "hetccl shim: abort: hetccl communicator released without device sync\n");
+    return;
   }
   hetccl_comm_destroy(hc);
 }
@@ -189,7 +216,7 @@ __attribute__((visibility("default"))) ncclResult_t ncclCommDestroy(ncclComm_t c
 }
 
 __attribute__((visibility("default"))) ncclResult_t ncclCommAbort(ncclComm_t comm) {
-  detach(comm);
+  detach(comm, true);
   return real<ncclResult_t (*)(ncclComm_t)>("ncclCommAbort")(comm);
 }
 

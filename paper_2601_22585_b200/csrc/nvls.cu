@@ -562,9 +562,11 @@ void nvls_buffer(const NvlsState* s, void** p, size_t* bytes) {
   if (bytes) *bytes = s ? s->ce_bytes : 0;
 }
 
-int nvls_supports(const NvlsState* s, int dt, int red, const void* send, const void* recv) {
-  if (!s || red != RED_SUM || !(dt == DT_BF16 || dt == DT_F16 || dt == DT_F32)) return 0;
-  return (((uintptr_t)send | (uintptr_t)recv) & 15) == 0;
+// The path choice depends only on values every rank shares (dtype, op), never on a rank's own pointers:
+// ranks that chose differently would wait on different flag arrays. Alignment is checked by the caller
+// (run_op), which rejects unaligned buffers in NVLS mode instead of switching path.
+int nvls_supports(const NvlsState* s, int dt, int red, const void*, const void*) {
+  return s && red == RED_SUM && (dt == DT_BF16 || dt == DT_F16 || dt == DT_F32);
 }
 
 cudaError_t nvls_allreduce(NvlsState* s, const void* send, void* recv, size_t count, int dt,

@@ -48,7 +48,8 @@ struct hetcclComm {
   int direct = 1;                         // HETCCL_DIRECT: write All-Reduce results straight into peers' recv
   int nslots = 8;                         // HETCCL_NSLOTS: scratch ring depth
   size_t os_bytes = 0;                    // HETCCL_ONESHOT_KB: one-shot AR up to this many bytes per rank
-  size_t os_stride = 0;                   // bytes per (buffer, sender) of the one-shot area
+  size_t os_chan = 0;                     // bytes per (buffer, sender, channel): each channel owns its region
+  size_t os_stride = 0;                   // bytes per (buffer, sender) of the one-shot area = nch_max * os_chan
   unsigned long long* trace = nullptr;
   size_t trace_bytes = 0;
   int trace_shape[2] = {0, 0};            // local ranks, channels of the last traced op
@@ -106,7 +107,15 @@ long env_long(const char* name, long dflt) {
   return e && *e ? atol(e) : dflt;
 }
 
-// [flags | base | nch_max x nslots slots | one-shot area: 2 buffers x n senders x os_stride]
+// [flags | base | nch_max x nslots slots | one-shot area: 2 buffers x n senders x nch_max channels x os_chan]
+// One-shot regions are private per channel: channel ch's double buffer (parity of ITS op counter) and its
+// ACK only order that channel's own reuse, so a region must never be shared between channels of different
+// ops (the channel count follows the message size).
+void set_os_layout(hetcclComm* c) {
+  const size_t per = (c->os_bytes + (size_t)c->nch_max - 1) / (size_t)c->nch_max;
+  c->os_chan = c->os_bytes ? (std::max<size_t>(per, 8192) + 256 + 255) / 256 * 256 : 0;
+  c->os_stride = (size_t)c->nch_max * c->os_chan;
+}
 size_t scratch_slots_bytes(const hetcclComm* c) { return (size_t)c->nch_max * c->nslots * c->slot_bytes; }
 size_t alloc_bytes_for(const hetcclComm* c) {
   return kFlagsReserve + scratch_slots_bytes(c) + 2 * (size_t)c->topo.n * c->os_stride;
@@ -130,7 +139,7 @@ void read_env(hetcclComm* c) {
   // (measured with CUDA graphs: 1+1 one-shot beats the pipeline up to 16 MiB; 2+2 up to ~4 MiB)
   const long os_default_kb = c->topo.n > 1 ? 16384L / (c->topo.n - 1) : 0;
   c->os_bytes = (size_t)std::max(0L, env_long("HETCCL_ONESHOT_KB", os_default_kb)) * 1024;
-  c->os_stride = (c->os_bytes + 255) / 256 * 256;
+  set_os_layout(c);
   c->alloc_bytes = alloc_bytes_for(c);
 }
 
@@ -212,16 +221,33 @@ hetcclResult_t run_op(hetcclComm_t c, int op, const void* const* sends, void* co
     const char* msg = check_overlap(op, sends[i], recvs[i], count, es, r, c->n);
     if (msg) return fail(c, hetcclInvalidArgument, "rank %d: %s", r, msg);
   }
+  // buffers must be device memory of the comm's device (else hetcclInvalidUsage)
+  for (int i = 0; i < nlocal; i++) {
+    const void* ps[2] = {sends[i], recvs[i]};
+    for (const void* p : ps) {
+      if (!p) continue;
+      cudaPointerAttributes at;
+      if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(c, hetcclInvalidUsage, "buffer %p is not CUDA memory", p);
+      }
+      if ((at.type != cudaMemoryTypeDevice && at.type != cudaMemoryTypeManaged) || at.device != c->device)
+        return fail(c, hetcclInvalidUsage, "buffer %p is not device memory of the comm's device %d (type %d, device %d)",
+                    p, c->device, (int)at.type, at.device);
+    }
+  }
   DevGuard g(c->device);
   if (c->n == 1) {  // a9: recv <- send
     if (recvs[0]) CUDA_TRY(c, launch_copy(sends[0], recvs[0], recv_elems(op, count, 1), es, stream));
     return hetcclSuccess;
   }
   if (op == OP_ALLREDUCE && c->nvls && nvls_supports(c->nvls, dt, red, sends[0], recvs[0])) {
+    if ((((uintptr_t)sends[0] | (uintptr_t)recvs[0]) & 15) != 0)
+      return fail(c, hetcclInvalidArgument, "NVLS mode needs 16-byte aligned send/recv buffers");
     CUDA_TRY(c, nvls_allreduce(c->nvls, sends[0], recvs[0], count, dt, c->err, c->timeout_ns, stream));
     return hetcclSuccess;
   }
-  const bool oneshot = op == OP_ALLREDUCE && c->os_bytes > 0 && count * (size_t)es <= c->os_bytes;
+  bool oneshot = op == OP_ALLREDUCE && c->os_bytes > 0 && count * (size_t)es <= c->os_bytes;
   OpArgs a;
   memset(&a, 0, sizeof(a));
   a.topo = c->topo;
@@ -245,11 +271,18 @@ hetcclResult_t run_op(hetcclComm_t c, int op, const void* const* sends, void* co
     nch_max = std::min(nch_max, cap / nlocal);
   }
   if (oneshot) {  // NEXT-3: one round trip; ~8 KiB of every rank's buffer per channel
+    a.nch = (int)std::max<size_t>(1, std::min<size_t>((size_t)nch_max, (count * (size_t)es + 8191) / 8192));
+    // the kernel's per-channel chunk (a multiple of the vector width) must fit the channel's private region
+    const size_t V = 16 / (size_t)es;
+    const size_t chunk = (count + (size_t)a.nch * V - 1) / ((size_t)a.nch * V) * V;
+    oneshot = chunk * (size_t)es <= c->os_chan && a.nch <= c->nch_max;
+  }
+  if (oneshot) {
     a.op = OP_ALLREDUCE_ONESHOT;
     a.count = count;
-    a.nch = (int)std::max<size_t>(1, std::min<size_t>((size_t)nch_max, (count * (size_t)es + 8191) / 8192));
     a.os_off = scratch_slots_bytes(c);
     a.os_stride = c->os_stride;
+    a.os_chan = c->os_chan;
     a.err = c->err;
     a.timeout_ns = c->timeout_ns;
     CUDA_TRY(c, launch_collective(a, nlocal, dt, red, c->kind == KIND_MUX, stream));
@@ -556,6 +589,7 @@ hetcclResult_t hetccl_comm_init_mux(hetcclComm_t* comm, int nranks, const int* r
     c->tile_base = (size_t)1 << 20;
     read_env(c);  // re-derive the slot from the larger tile
     c->nch_max = std::max(1, std::min(c->nch_max, sms * kCtasPerSm / nranks));
+    set_os_layout(c);
     c->alloc_bytes = alloc_bytes_for(c);
   }
   cudaError_t e = cudaSuccess;

@@ -101,3 +101,44 @@ def test_oneshot_multi(name):
     finally:
         for c in comms:
             hc.hetccl_comm_destroy(c)
+
+
+@pytest.mark.multigpu
+@pytest.mark.parametrize("name", ["1+1", "2+2", "1+1+2"])
+def test_oneshot_multi_back_to_back_mixed_sizes(name):
+    """one-shot ops of different sizes use different channel counts; enqueued back to back
+    on every GPU with no host sync, a fast rank's next op must never overwrite a region a slow peer is still
+    reading. Each channel now owns a private region, so its own parity + ACK order every reuse. Every op has
+    its own output buffers and all results are checked after the whole sequence."""
+    import torch
+    hc = _hc()
+    m = MAPS[name]
+    n = len(m)
+    if torch.cuda.device_count() < n:
+        pytest.skip(f"needs {n} GPUs")
+    comms = hc.hetccl_comm_init_all(list(range(n)), m)
+    try:
+        sizes = [2000, 6000, 8192, 3000, 16000, 24577, 4096, 100, 70000, 5000] * 4
+        cases = []
+        for i, count in enumerate(sizes):
+            xs = inputs("normal", 700 + i, n, count, "bf16")
+            sends = [to_torch(xs[r], "bf16", f"cuda:{r}") for r in range(n)]
+            recvs = [torch.empty_like(s) for s in sends]
+            cases.append((xs, sends, recvs))
+        streams = [torch.cuda.Stream(device=r) for r in range(n)]
+        for r in range(n):
+            torch.cuda.synchronize(r)
+        for r in range(n):  # rank r enqueues its whole sequence before rank r+1 starts: maximal skew
+            for xs, sends, recvs in cases:
+                hc.allreduce(sends[r], recvs[r], comms[r], stream=streams[r])
+        for r in range(n):
+            torch.cuda.synchronize(r)
+        for c in comms:
+            hc.hetccl_comm_get_async_error(c)
+        for i, (xs, sends, recvs) in enumerate(cases):
+            want = oracle.allreduce(xs, m, "bf16", "sum")
+            for r in range(n):
+                assert np.array_equal(to_numpy(recvs[r], "bf16"), want), f"op {i} (count {sizes[i]}) rank {r}"
+    finally:
+        for c in comms:
+            hc.hetccl_comm_destroy(c)

@@ -65,3 +65,27 @@ def test_special_values(name, dt, oneshot, monkeypatch):
             assert np.array_equal(gb[~wn], wb[~wn]), f"{name} {dt} rank {r}: non-NaN values differ"
     finally:
         hc.hetccl_comm_destroy(comm)
+
+
+def test_buffers_must_be_device_memory_of_the_comm():
+    """a host buffer (or one on another device) is hetcclInvalidUsage, checked before launch."""
+    import torch
+    import paper_2601_22585_b200 as hc
+    comm = hc.hetccl_comm_init_mux(2, [0, 1], 0)
+    try:
+        dev = [torch.zeros(4096, device="cuda") for _ in range(2)]
+        host = [torch.zeros(4096).pin_memory() for _ in range(2)]
+        plain = [torch.zeros(4096) for _ in range(2)]
+        for bad_s, bad_r in ((host, dev), (dev, host), (plain, dev)):
+            with pytest.raises(hc.HetcclError) as ei:
+                hc.mux_allreduce(bad_s, bad_r, comm)
+            assert ei.value.code == 5, ei.value
+        if torch.cuda.device_count() > 1:
+            other = [torch.zeros(4096, device="cuda:1") for _ in range(2)]
+            with pytest.raises(hc.HetcclError) as ei:
+                hc.mux_allreduce(other, dev, comm)
+            assert ei.value.code == 5
+        hc.mux_allreduce(dev, dev, comm)  # still usable
+        torch.cuda.synchronize()
+    finally:
+        hc.hetccl_comm_destroy(comm)
