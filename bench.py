@@ -112,6 +112,64 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
+class NvlinkCounter:
+    """NVLink bytes this GPU transmitted / received, summed over its links, from NVML field values read
+    before and after the timed region (the hardware counter behind "achieved NVLink GB/s"). Tries the
+    byte counters (NVML_FI_DEV_NVLINK_COUNT_XMIT/RCV_BYTES) and falls back to the data-throughput counters
+    (NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX/RX, KiB); reports which one it used, or why none worked."""
+    FIELDS = ((202, 204, 1, "NVML_FI_DEV_NVLINK_COUNT_XMIT/RCV_BYTES"),
+              (138, 139, 1024, "NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX/RX (KiB)"))
+
+    def __init__(self, cuda_device):
+        self.err, self.h, self.field = None, None, None
+        try:
+            import pynvml
+            import torch
+            self.nv = pynvml
+            pynvml.nvmlInit()
+            pr = torch.cuda.get_device_properties(cuda_device)
+            bus = f"{pr.pci_domain_id:08X}:{pr.pci_bus_id:02X}:{pr.pci_device_id:02X}.0"
+            self.h = pynvml.nvmlDeviceGetHandleByPciBusId_v2(bus)
+            self.links = []
+            for l in range(pynvml.NVML_NVLINK_MAX_LINKS):
+                try:
+                    if pynvml.nvmlDeviceGetNvLinkState(self.h, l) == pynvml.NVML_FEATURE_ENABLED:
+                        self.links.append(l)
+                except Exception:
+                    pass
+            for tx, rx, scale, name in self.FIELDS:
+                if self._read(tx, rx, scale) is not None:
+                    self.field = (tx, rx, scale, name)
+                    break
+            if self.field is None:
+                self.err = f"no NVLink byte counter readable ({len(self.links)} links up)"
+        except Exception as e:  # no NVML / no NVLink: report, do not fail the bench
+            self.err = f"{type(e).__name__}: {e}"
+
+    def _read(self, tx, rx, scale):
+        try:
+            req = [(tx, l) for l in self.links] + [(rx, l) for l in self.links]
+            vals = self.nv.nvmlDeviceGetFieldValues(self.h, req)
+            if not vals or any(v.nvmlReturn != 0 for v in vals):
+                return None
+            k = len(self.links)
+            return (sum(int(v.value.ullVal) for v in vals[:k]) * scale,
+                    sum(int(v.value.ullVal) for v in vals[k:]) * scale)
+        except Exception:
+            return None
+
+    def sample(self):
+        return self._read(*self.field[:3]) if self.field else None
+
+    def delta(self, a, b, seconds, steps):
+        if self.field is None or a is None or b is None:
+            return {"available": False, "why": self.err or "counter read failed"}
+        tx, rx = b[0] - a[0], b[1] - a[1]
+        return {"available": True, "counter": self.field[3], "links": len(self.links),
+                "tx_bytes_per_step": tx // max(1, steps), "rx_bytes_per_step": rx // max(1, steps),
+                "tx_GBps": round(tx / seconds / 1e9, 2), "rx_GBps": round(rx / seconds / 1e9, 2)}
+
+
 def profiled_traffic(key):
     """DRAM bytes per launch of the dominant kernel from the committed ncu --set full capture
     (profiles/ncu_traffic.json, written by tools/ncu_summary.py), or None."""
@@ -128,24 +186,33 @@ def busbw(nbytes, t_s, n):
     return alg, alg * 2 * (n - 1) / n
 
 
-def oracle_baseline(xs_host, m, recv_dev_list, budget_s=20.0):
-    """cpu_baseline leg: the oracle as it stands, single thread, on a bounded sample of the workload; the
-    GPU result on the same sample is compared with it bitwise (the only place bench.py runs oracle/)."""
+def oracle_baseline(xs_host, m, recv_dev_list, budget_s=15.0):
+    """cpu_baseline leg: the oracle as it stands on a bounded sample of the workload, timed twice — on one
+    host thread and on every host core (oracle.allreduce_threaded: elements split across threads, same
+    per-element fold, bit-identical) — and the GPU result on the same sample compared with it bitwise (the
+    only place bench.py runs oracle/ besides --impl reference). `value`/`cores` are the all-cores run."""
     import oracle
     import torch
     count = xs_host[0].size
-    # ~40 ns/element for 8 ranks: bound the sample to the budget
-    sample = int(min(count, max(1 << 16, budget_s / 45e-9)))
+    # ~15 ns per element index for 8 ranks single-threaded: bound the sample to the budget
+    sample = int(min(count, max(1 << 16, budget_s / (2e-9 * len(m)))))
     xs = [x[:sample] for x in xs_host]
     t0 = time.perf_counter()
     want = oracle.allreduce(xs, m, "bf16", "sum")
-    dt = time.perf_counter() - t0
-    alg, bus = busbw(sample * 2, dt, len(m))
-    ok = all(bool(np.array_equal(y[:sample].cpu().view(torch.int16).numpy().view(np.uint16), want))
-             for y in recv_dev_list)
-    return {"value": round(bus, 3), "unit": "GB/s", "cores": 1, "kind": "oracle",
+    dt1 = time.perf_counter() - t0
+    cores = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    want_t = oracle.allreduce_threaded(xs, m, "bf16", "sum", threads=cores)
+    dtt = time.perf_counter() - t0
+    _, bus1 = busbw(sample * 2, dt1, len(m))
+    _, bust = busbw(sample * 2, dtt, len(m))
+    ok = bool(np.array_equal(want, want_t)) and all(
+        bool(np.array_equal(y[:sample].cpu().view(torch.int16).numpy().view(np.uint16), want)) for y in recv_dev_list)
+    return {"value": round(bust, 3), "unit": "GB/s", "cores": cores, "kind": "oracle",
             "sample": f"first {sample} of {count} elements per rank, all {len(m)} ranks, one All-Reduce "
-                      f"({dt:.2f} s single-threaded); busbw convention as value",
+                      f"({dtt:.2f} s on {cores} host threads, elements split across threads; {dt1:.2f} s on 1); "
+                      f"busbw convention as value",
+            "single_thread": {"value": round(bus1, 3), "unit": "GB/s", "cores": 1},
             "gpu_bitwise_equal_on_sample": ok}
 
 
@@ -318,8 +385,16 @@ def run_dist(args):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    nvc = NvlinkCounter(local)
     with ClockSampler(local) as clk:
+        c0 = nvc.sample()
         total_ms, launch_ms = timed(step, args.steps)
+        c1 = nvc.sample()
+    nvl = nvc.delta(c0, c1, total_ms * 1e-3, args.steps)
+    # busiest rank's measured NVLink transmit bytes per launch (max over ranks)
+    txm = torch.tensor([float(nvl.get("tx_bytes_per_step", -1))], device="cuda")
+    dist.all_reduce(txm, op=dist.ReduceOp.MAX)
+    nvl["tx_bytes_per_step_max_over_ranks"] = int(txm.item())
     # staged path (plain torch recv buffer) for comparison
     for _ in range(args.warmup):
         hc.allreduce(send_plain, recv_staged, comm, stream=sp)
@@ -358,10 +433,16 @@ def run_dist(args):
     e2e_ms, _ = timed(e2e_step, e2e_steps)
     _, e2e_bus = busbw(S, e2e_ms / e2e_steps * 1e-3, world)
 
-    plan = hc.hetccl_plan_info(m, rank, hc.OP_ALLREDUCE, count, hc.BFLOAT16)
     busiest = max(hc.hetccl_plan_info(m, r, hc.OP_ALLREDUCE, count, hc.BFLOAT16)["bytes_sent"] for r in range(world))
     achieved = busiest / (launch_ms * 1e-3) / 1e9
     clocks = clk.summary()
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        # the oracle on a bounded sample: every rank's first elements regenerated from the generator; checked
+        # bitwise against this rank's GPU result on the same elements
+        ns = min(count, 1 << 22)
+        cpu = oracle_baseline([synth.normal(SEED, r, ns, "bf16") for r in range(world)], m, [recv[:ns]])
+    dist.barrier()
     hc.hetccl_comm_destroy(comm)
     if rank == 0:
         out = {
@@ -378,12 +459,16 @@ def run_dist(args):
             "e2e": {"value": round(e2e_bus, 2), "unit": "GB/s", "h2d_bytes_per_step": world * S,
                     "d2h_bytes_per_step": world * S},
             "roofline": {"bound": "nvlink", "achieved": round(achieved, 1), "peak": NVLINK_PEAK, "unit": "GB/s",
-                         "frac": round(achieved / NVLINK_PEAK, 4), "traffic": None,
+                         "frac": round(achieved / NVLINK_PEAK, 4),
+                         "traffic": nvl.get("tx_bytes_per_step_max_over_ranks") if nvl.get("available") else None,
                          "note": f"algorithmic = busiest rank's NVLink bytes sent per launch ({busiest} B, plan) / "
-                                 f"avg k_allreduce launch {launch_ms:.4f} ms; peak = measured peer copy per direction"},
+                                 f"avg k_allreduce launch {launch_ms:.4f} ms; peak = measured peer copy per direction; "
+                                 f"traffic = NVLink bytes transmitted per launch, max over ranks (NVML counter, "
+                                 f"this run; an ncu DRAM capture cannot wrap a multi-rank command)"},
+            "nvlink_counters": nvl,
             "parity": {"ok": bool(okt.item()), "how": "R7 gate vs fp64 sum on 3 windows x 4096 elements, all ranks"},
             "clocks": clocks,
-            "cpu_baseline": None,
+            "cpu_baseline": cpu,
         }
         print(json.dumps(out), flush=True)
     dist.barrier()

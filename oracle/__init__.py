@@ -110,6 +110,36 @@ def allreduce(xs, rank_to_domain, dtype, op="sum"):
     return y
 
 
+def allreduce_threaded(xs, rank_to_domain, dtype, op="sum", threads=None):
+    """allreduce() with the ELEMENTS split into `threads` contiguous ranges, each reduced by one host thread
+    calling the same C routine on its range (ctypes releases the GIL). The per-element fold order is
+    unchanged ("an optional T-thread variant splits elements only"), so Y is bit-identical to
+    allreduce(). Used for the T = host-cores oracle timing beside the GPU."""
+    from concurrent.futures import ThreadPoolExecutor
+    dt, o = _dt(dtype), _op(op)
+    xs = _check(xs, dt, xs[0].size)
+    count = xs[0].size
+    y = np.empty(count, NP_DTYPE[dt])
+    T = max(1, min(int(threads or os.cpu_count() or 1), count))
+    es = y.itemsize
+    bounds = [count * t // T for t in range(T + 1)]
+    m = _map(rank_to_domain)
+    L = lib()
+
+    def run(t):
+        lo, hi = bounds[t], bounds[t + 1]
+        if hi <= lo:
+            return 0
+        ptrs = (ctypes.c_void_p * len(xs))(*[x.ctypes.data + lo * es for x in xs])
+        return L.oracle_allreduce(len(xs), m, ptrs, y.ctypes.data + lo * es, hi - lo, dt, o)
+
+    with ThreadPoolExecutor(max_workers=T) as ex:
+        rcs = list(ex.map(run, range(T)))
+    if any(rcs):
+        raise ValueError("oracle_allreduce: invalid argument")
+    return y
+
+
 def reduce_scatter(xs, rank_to_domain, dtype, op="sum"):
     """[y_0 .. y_{n-1}]: rank r's block r of the reduction (x_r holds n*recvcount elements)."""
     dt, o = _dt(dtype), _op(op)

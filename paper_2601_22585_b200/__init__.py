@@ -141,6 +141,8 @@ def _stream(stream, like=None):
     if stream is None:
         import torch
         dev = like.device if like is not None and hasattr(like, "device") else None
+        if dev is not None and dev.type != "cuda":
+            dev = None  # a host tensor: the library rejects it (hetcclInvalidUsage); any stream will do
         return torch.cuda.current_stream(dev).cuda_stream
     if isinstance(stream, int):
         return stream

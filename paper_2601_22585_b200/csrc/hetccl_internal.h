@@ -20,15 +20,16 @@ namespace hetccl {
 
 constexpr int kMaxRanks = 16;      // == HETCCL_MAX_RANKS (one flag line = 16 senders x 8 B)
 #ifndef HETCCL_CTAS_PER_SM
-#define HETCCL_CTAS_PER_SM 2
+#define HETCCL_CTAS_PER_SM 4
 #endif
-constexpr int kCtasPerSm = HETCCL_CTAS_PER_SM;     // resident CTAs per SM the kernels are built for
+constexpr int kCtasPerSm = HETCCL_CTAS_PER_SM;     // resident CTAs per SM the kernels are built for (<= 128 registers)
 constexpr int kMaxChannels = 148 * kCtasPerSm;     // hard cap on CTAs per rank per op
+constexpr int kDefaultChannels = 296;              // channels of a one-rank-per-GPU comm unless HETCCL_NCHANNELS
 constexpr int kMaxSlots = 16;      // cap on the scratch ring depth per channel (HETCCL_NSLOTS)
 #ifndef HETCCL_THREADS
 #define HETCCL_THREADS 128
 #endif
-constexpr int kThreads = HETCCL_THREADS;  // threads per CTA (one CTA per SM)
+constexpr int kThreads = HETCCL_THREADS;  // threads per CTA (kCtasPerSm CTAs per SM)
 constexpr int kMaxStages = 5;      // pipeline positions of the deepest op (All-Reduce)
 constexpr int kTraceWords = 8;     // per traced iteration: poll start, GO, DONE, fenced, end of stages 0..3
 
@@ -122,6 +123,7 @@ struct OpArgs {
   int flat_ag;                  // 1 (with direct): C writes each final piece into EVERY rank's recv (no stage D)
   int pull;                     // 1 (with direct): every rank's send buffer is addressable (peer_send): the domain
   const void* peer_send[kMaxRanks];  // fold reads peers' x directly, stage A and the s1 staging vanish
+  int tma;                      // 1: the movers stage their sources through the TMA ring (dynamic shared memory)
 };
 
 // ---- host plan (plan.cpp) ----

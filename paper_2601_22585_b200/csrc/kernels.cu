@@ -210,8 +210,11 @@ __device__ __forceinline__ void prefetch_ahead(const void* src, size_t v0, int t
                : "memory");
 }
 
+#ifndef HETCCL_TMA
+#define HETCCL_TMA 1
+#endif
 #ifndef HETCCL_STAGE_SMEM
-#define HETCCL_STAGE_SMEM 1
+#define HETCCL_STAGE_SMEM (!HETCCL_TMA)  // the TMA ring replaces the cp.async staging (shared memory budget)
 #endif
 // Fold sources are staged through shared memory with cp.async (LDGSTS): each data thread issues the
 // 16-byte loads of up to kStageSrc sources x kUnroll vectors at once and waits once, so a fold keeps
@@ -230,6 +233,192 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
 }
 
+// ------------------------------------------------------------------ TMA-staged movers ----------
+// The pipeline kernels' data movers stream their sources through a ring of kTmaStages shared-memory
+// stages filled by TMA bulk copies (cp.async.bulk global->shared; completion counted on the stage's FULL
+// mbarrier): the first data thread keeps kTmaStages-1 chunks of every operand in flight while every data
+// warp folds the oldest chunk out of shared memory and stores the result (16-byte st.global, to every
+// destination), then arrives on the stage's EMPTY mbarrier; the producer refills a stage once every data
+// warp has arrived. No CTA-wide barrier per chunk: a warp only waits for its data, the producer only for
+// the slowest warp of the chunk NST-1 behind. Loads cost no registers or issue slots of the folding
+// threads, so the bytes in flight per CTA (~3 x 24 KiB) do not depend on the register budget (the
+// LDG/LDGSTS movers of round 1 kept 12% of warps active at 254 registers, profiles/r01/q28). Operand and
+// destination pointers live in shared memory for the duration of a call (the PtrLists are on the stack,
+// and their local-memory reads missed L1 once the ring took the shared-memory carve-out: r02e).
+//   chunk g of this CTA (g counts every chunk of every mover call since kernel start, g_seq) uses stage
+//   g % kTmaStages; it is that stage's u-th use (u = g / kTmaStages): FULL phase parity u & 1, and before
+//   issuing it the producer waits for EMPTY completion u-1 (parity (u-1) & 1).
+#ifndef HETCCL_TMA_STAGES
+#define HETCCL_TMA_STAGES 3
+#endif
+#ifndef HETCCL_TMA_STAGE_KB
+#define HETCCL_TMA_STAGE_KB 16  // 3 x 16 KiB per CTA, 4 CTAs per SM (r02k: 2 CTAs x 4 x 24 KiB -10%)
+#endif
+constexpr int kTmaStages = HETCCL_TMA_STAGES;
+constexpr int kTmaStageBytes = HETCCL_TMA_STAGE_KB * 1024;
+constexpr int kTmaMaxVpt = 4;  // 16-byte vectors per thread per operand per chunk (register bound of the fold)
+#ifndef HETCCL_TMA_ALIGN_V
+#define HETCCL_TMA_ALIGN_V 8
+#endif
+constexpr uint32_t kTmaAlignV = HETCCL_TMA_ALIGN_V;  // chunk granularity in 16-byte vectors
+__shared__ __align__(8) uint64_t g_full[kTmaStages];
+__shared__ __align__(8) uint64_t g_empty[kTmaStages];
+__shared__ unsigned g_seq;  // chunks this CTA has issued/consumed so far (all data threads agree)
+__shared__ int g_tma;       // 1: the ring is initialised and the op may use it
+__shared__ const char* g_ops[kMaxList + kMaxRanks];  // operands of the current call, in load order
+__shared__ char* g_dst[kMaxList];                     // destinations of the current call
+extern __shared__ __align__(128) unsigned char g_ring[];
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok)
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(ok)
+                 : "r"(smem_addr(b)), "r"(parity)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr(sdst)),
+               "l"(gsrc), "r"(bytes), "r"(smem_addr(b))
+               : "memory");
+}
+__device__ __forceinline__ void data_bar() { asm volatile("bar.sync 1, %0;" ::"r"(g_dnth) : "memory"); }
+
+// thread 0 at the start of a pipeline kernel, before its first __syncthreads (data warps: all warps, or
+// all but the sync warp in the warp-specialised mode)
+__device__ __forceinline__ void tma_init(int enable, int data_warps) {
+  if (threadIdx.x == 0) {
+    g_tma = HETCCL_TMA && enable;
+    g_seq = 0;
+    if (g_tma) {
+      for (int s = 0; s < kTmaStages; s++) {
+        mbar_init(&g_full[s], 1);
+        mbar_init(&g_empty[s], (uint32_t)data_warps);
+      }
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+  }
+}
+
+// operands the ring can stage (at least one warp's vectors of each per chunk), nv vectors in 32 bits
+__device__ __forceinline__ bool tma_fits(int nops, size_t nv) {
+  return g_tma && nops >= 1 && nops <= kMaxList + kMaxRanks && nops * 16 * (int)max(32u, kTmaAlignV) <= kTmaStageBytes &&
+         nv < (1u << 31);
+}
+
+// Chunk loop of the movers: operands g_ops[0..nops), destinations g_dst[0..nd) (shared memory), nv
+// 16-byte vectors. Kept free of stack state (scalar arguments, 32-bit counters, pointers from shared
+// memory): with the ring holding most of the shared-memory carve-out the L1 left for local memory is
+// small, and one spilled loop variable reloaded from L2 per chunk cost ~a quarter of the kernel (r02g).
+template <typename T, int OP, int MODE>
+__device__ __noinline__ void tma_stream(int ni, int D, int kpos, int nd, uint32_t nv, unsigned seq0) {
+  using TR = Tr<T>;
+  using S = typename TR::S;
+  using A = typename TR::A;
+  constexpr int V = TR::V;
+  const int tid = (int)threadIdx.x - g_dbase, nth = g_dnth;
+  const int nops = MODE == 2 ? ni + D - 1 : (MODE == 1 ? ni : 1);
+  // vectors per operand per chunk: as many as the stage holds, in whole 128-byte lines (HETCCL_TMA_ALIGN_V
+  // vectors) so every bulk copy starts line-aligned in global memory when the operand does
+  const uint32_t cv = min((uint32_t)(kTmaStageBytes / (nops * 16)) / kTmaAlignV * kTmaAlignV, (uint32_t)(kTmaMaxVpt * nth));
+  const uint32_t chb = cv * 16;
+  const uint32_t nchunks = (nv + cv - 1) / cv;
+  const uint32_t ring = smem_addr(g_ring), full = smem_addr(g_full), empty = smem_addr(g_empty);
+  if (tid == 0) {
+    for (uint32_t c = 0; c < nchunks && c < (uint32_t)kTmaStages - 1; c++) {
+      const unsigned g = seq0 + c, st = g % kTmaStages, u = g / kTmaStages;
+      if (u > 0) mbar_wait(&g_empty[st], (u - 1) & 1u);
+      const uint32_t bytes = min(cv, nv - c * cv) * 16;
+      mbar_arrive_expect_tx(&g_full[st], bytes * (uint32_t)nops);
+      for (int j = 0; j < nops; j++) bulk_g2s(g_ring + st * kTmaStageBytes + j * chb, g_ops[j] + (size_t)c * chb, bytes, &g_full[st]);
+    }
+  }
+  (void)ring;
+  (void)full;
+  (void)empty;
+  const int lane = threadIdx.x & 31;
+  for (uint32_t c = 0; c < nchunks; c++) {
+    if (tid == 0 && c + kTmaStages - 1 < nchunks) {
+      const uint32_t cn = c + kTmaStages - 1;
+      const unsigned g = seq0 + cn, st = g % kTmaStages, u = g / kTmaStages;
+      if (u > 0) mbar_wait(&g_empty[st], (u - 1) & 1u);  // every data warp is done with the stage's last use
+      const uint32_t bytes = min(cv, nv - cn * cv) * 16;
+      mbar_arrive_expect_tx(&g_full[st], bytes * (uint32_t)nops);
+      for (int j = 0; j < nops; j++) bulk_g2s(g_ring + st * kTmaStageBytes + j * chb, g_ops[j] + (size_t)cn * chb, bytes, &g_full[st]);
+    }
+    const unsigned g = seq0 + c, st = g % kTmaStages;
+    mbar_wait(&g_full[st], (g / kTmaStages) & 1u);
+    const unsigned char* sb = g_ring + st * kTmaStageBytes;
+    const uint32_t lim = min(cv, nv - c * cv);
+    for (uint32_t idx = tid; idx < lim; idx += nth) {
+      uint4 o = *(const uint4*)(sb + idx * 16);
+      if (MODE != 0) {
+        // first operand peeled (no loop-carried "first?" select: it pushed acc[] to local memory, r02j)
+        A acc[V];
+#pragma unroll
+        for (int e = 0; e < V; e++) acc[e] = TR::widen(Vec<S>::get(o, e));
+#pragma unroll 1
+        for (int j = 1; j < ni; j++) {
+          const uint4 w = *(const uint4*)(sb + j * chb + idx * 16);
+#pragma unroll
+          for (int e = 0; e < V; e++) acc[e] = comb<OP>(acc[e], TR::widen(Vec<S>::get(w, e)));
+        }
+        if (MODE == 2) {
+          uint4 pk;
+#pragma unroll
+          for (int e = 0; e < V; e++) Vec<S>::set(pk, e, TR::narrow(acc[e]));
+          const uint4 w0 = kpos == 0 ? pk : *(const uint4*)(sb + ni * chb + idx * 16);
+#pragma unroll
+          for (int e = 0; e < V; e++) acc[e] = TR::widen(Vec<S>::get(w0, e));
+#pragma unroll 1
+          for (int q = 1; q < D; q++) {
+            const uint4 w = q == kpos ? pk : *(const uint4*)(sb + (ni + (q < kpos ? q : q - 1)) * chb + idx * 16);
+#pragma unroll
+            for (int e = 0; e < V; e++) acc[e] = comb<OP>(acc[e], TR::widen(Vec<S>::get(w, e)));
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < V; e++) Vec<S>::set(o, e, TR::narrow(acc[e]));
+      }
+      const size_t off = ((size_t)c * cv + idx) * 16;
+      for (int d = 0; d < nd; d++) st_v4(g_dst[d] + off, o);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&g_empty[st]);  // this warp is done with stage st
+  }
+  *(volatile unsigned*)&g_seq = seq0 + nchunks;  // every data thread writes the same value
+}
+
+// Vector part (nv 16-byte vectors) of the three movers through the ring:
+//   MODE 0 copy : dst[d] = inner[0] (bits)
+//   MODE 1 fold : dst[d] = narrow(fold_{s} widen(inner[s]))
+//   MODE 2 hier : P = narrow(fold_s widen(inner[s])); dst[d] = narrow(fold_{q < outer.n} widen(q == kpos ? P : outer[q]))
+// Operands are staged in load order inner[0..ni), then outer[q] for q != kpos ascending.
+template <typename T, int OP, int MODE>
+__device__ __forceinline__ void tma_move(const PtrList& inner, int kpos, const PtrList& outer, const PtrList& dsts,
+                                         size_t nv) {
+  const int tid = (int)threadIdx.x - g_dbase;
+  const int ni = inner.n, D = outer.n, nd = dsts.n;
+  const int nops = MODE == 2 ? ni + D - 1 : (MODE == 1 ? ni : 1);
+  data_bar();  // every data thread is done with the previous call's pointers and has published g_seq
+  const unsigned seq0 = *(volatile unsigned*)&g_seq;  // read before the 2nd barrier: no thread can move it on yet
+  if (tid < nops) g_ops[tid] = (const char*)(tid < ni ? inner.p[tid] : outer.p[tid - ni < kpos ? tid - ni : tid - ni + 1]);
+  if (tid < nd) g_dst[tid] = (char*)dsts.p[tid];
+  data_bar();
+  tma_stream<T, OP, MODE>(ni, D, kpos, nd, (uint32_t)nv, seq0);
+}
+
 // dst[d][i] = src[i] for every destination d, i < n elements of size ES (bit copy)
 template <int ES>
 __device__ __noinline__ void cta_copy(const void* src, const PtrList& dsts, size_t n) {
@@ -240,7 +429,13 @@ __device__ __noinline__ void cta_copy(const void* src, const PtrList& dsts, size
   s1.add(src);
   const size_t nv = all_aligned16(s1, dsts) ? n / V : 0;
   const char* sp = (const char*)src;
-  for (size_t v0 = tid; v0 < nv; v0 += (size_t)kCopyUnroll * nth) {
+  size_t nvr = nv;  // vectors left to the register path
+  if (nv && tma_fits(1, nv)) {
+    PtrList none;
+    tma_move<float, RED_SUM, 0>(s1, -1, none, dsts, nv);
+    nvr = 0;
+  }
+  for (size_t v0 = tid; v0 < nvr; v0 += (size_t)kCopyUnroll * nth) {
     prefetch_ahead(sp, v0, tid, (size_t)kCopyUnroll * nth, nv);
     uint4 w[kCopyUnroll];
 #pragma unroll
@@ -289,8 +484,14 @@ __device__ __noinline__ void cta_fold(const PtrList& srcs, const PtrList& dsts, 
   }
   const int tid = (int)threadIdx.x - g_dbase, nth = g_dnth;
   const size_t nv = all_aligned16(srcs, dsts) ? n / V : 0;
+  size_t nvr = nv;  // vectors left to the register path
+  if (nv && tma_fits(srcs.n, nv)) {
+    PtrList none;
+    tma_move<T, OP, 1>(srcs, -1, none, dsts, nv);
+    nvr = 0;
+  }
 #if HETCCL_STAGE_SMEM
-  for (size_t v0 = tid; v0 < nv; v0 += (size_t)kUnroll * nth) {
+  for (size_t v0 = tid; v0 < nvr; v0 += (size_t)kUnroll * nth) {
     for (int s = 0; s < srcs.n; s++) prefetch_ahead(srcs.p[s], v0, tid, (size_t)kUnroll * nth, nv);
     A acc[kUnroll][V];
     for (int s0 = 0; s0 < srcs.n; s0 += kStageSrc) {
@@ -317,7 +518,7 @@ __device__ __noinline__ void cta_fold(const PtrList& srcs, const PtrList& dsts, 
       }
     }
 #else
-  for (size_t v0 = tid; v0 < nv; v0 += (size_t)kUnroll * nth) {
+  for (size_t v0 = tid; v0 < nvr; v0 += (size_t)kUnroll * nth) {
     for (int s = 0; s < srcs.n; s++) prefetch_ahead(srcs.p[s], v0, tid, (size_t)kUnroll * nth, nv);
     A acc[kUnroll][V];
     {
@@ -397,6 +598,11 @@ __device__ __noinline__ void cta_fold_hier(const PtrList& inner, int kpos, const
   for (int q = 0; q < D; q++)
     if (q != kpos) al |= (uintptr_t)outer.p[q];
   const size_t nv = (all_aligned16(inner, dsts) && (al & 15) == 0) ? n / V : 0;
+  size_t nvr = nv;  // vectors left to the register path
+  if (nv && tma_fits(inner.n + D - 1, nv)) {
+    tma_move<T, OP, 2>(inner, kpos, outer, dsts, nv);
+    nvr = 0;
+  }
 #if HETCCL_STAGE_SMEM
   // operand list in load order: inner[0..inner.n), then outer[q] for q != kpos ascending; staged in groups
   // of kStageSrc (at 4+4 all five operands of a tile batch are in flight at once)
@@ -406,7 +612,7 @@ __device__ __noinline__ void cta_fold_hier(const PtrList& inner, int kpos, const
     const int q = j - inner.n;
     return (const char*)outer.p[q < kpos ? q : q + 1];
   };
-  for (size_t v0 = tid; v0 < nv; v0 += (size_t)kUnroll * nth) {
+  for (size_t v0 = tid; v0 < nvr; v0 += (size_t)kUnroll * nth) {
     for (int s = 0; s < inner.n; s++) prefetch_ahead(inner.p[s], v0, tid, (size_t)kUnroll * nth, nv);
     for (int q = 0; q < D; q++)
       if (q != kpos) prefetch_ahead(outer.p[q], v0, tid, (size_t)kUnroll * nth, nv);
@@ -468,7 +674,7 @@ __device__ __noinline__ void cta_fold_hier(const PtrList& inner, int kpos, const
       }
     }
 #else
-  for (size_t v0 = tid; v0 < nv; v0 += (size_t)kUnroll * nth) {
+  for (size_t v0 = tid; v0 < nvr; v0 += (size_t)kUnroll * nth) {
     for (int s = 0; s < inner.n; s++) prefetch_ahead(inner.p[s], v0, tid, (size_t)kUnroll * nth, nv);
     for (int q = 0; q < D; q++)
       if (q != kpos) prefetch_ahead(outer.p[q], v0, tid, (size_t)kUnroll * nth, nv);
@@ -799,6 +1005,7 @@ __device__ __forceinline__ void run_pipeline(const OpArgs& a, Op& op, int me, in
   P.npos = P.SP * (P.np - 1) + 1;
   if (threadIdx.x < kCounters * kMaxRanks)
     ps.base[threadIdx.x / kMaxRanks][threadIdx.x % kMaxRanks] = B[threadIdx.x / kMaxRanks * kLineWords + threadIdx.x % kMaxRanks];
+  tma_init(a.tma, (a.ws >= 2 ? (int)blockDim.x - 32 : (int)blockDim.x) / 32);
   if (threadIdx.x == 0) {
     ps.tiles0 = B[kCounters * kLineWords];
     ps.abort_ = 0;
@@ -1543,6 +1750,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_allreduce_oneshot(cons
     g_dbase = 0;
     g_dnth = blockDim.x;
     g_pf = 1;
+    g_tma = 0;  // no ring in the one-shot kernel (its movers take the register path)
   }
   __syncthreads();
   const unsigned long long g = ops0;
@@ -1677,13 +1885,24 @@ static KernFn pick(int op, int dt, int red) {
   return nullptr;
 }
 
+// dynamic shared memory of a launch: the TMA ring for the pipeline kernels when the op uses it
+static size_t dyn_smem(int op, int tma) { return (HETCCL_TMA && tma && op != OP_ALLREDUCE_ONESHOT) ? (size_t)kTmaStages * kTmaStageBytes : 0; }
+
+static cudaError_t allow_smem(KernFn fn, size_t bytes) {
+  if (bytes == 0) return cudaSuccess;  // (static + dynamic > 48 KiB needs the opt-in even for 48 KiB dynamic)
+  return cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
 cudaError_t launch_collective(const OpArgs& a, int nlocal, int dt, int red, bool cooperative, cudaStream_t s) {
   KernFn fn = a.op == OP_ALLREDUCE_ONESHOT ? pick_oneshot(dt, red) : pick(a.op, dt, red);
   if (!fn) return cudaErrorInvalidValue;
+  const size_t smem = dyn_smem(a.op, a.tma);
+  cudaError_t e = allow_smem(fn, smem);
+  if (e != cudaSuccess) return e;
   dim3 grid(a.nch, nlocal), block(kThreads);
   void* args[] = {(void*)&a};
-  if (cooperative) return cudaLaunchCooperativeKernel((const void*)fn, grid, block, args, 0, s);
-  return cudaLaunchKernel((const void*)fn, grid, block, args, 0, s);
+  if (cooperative) return cudaLaunchCooperativeKernel((const void*)fn, grid, block, args, smem, s);
+  return cudaLaunchKernel((const void*)fn, grid, block, args, smem, s);
 }
 
 cudaError_t launch_copy(const void* src, void* dst, size_t n, int es, cudaStream_t s) {
@@ -1697,12 +1916,14 @@ cudaError_t launch_copy(const void* src, void* dst, size_t n, int es, cudaStream
 }
 
 // max co-resident CTAs of a collective kernel on this device (for the cooperative mux launch)
-int max_coresident(int op, int dt, int red) {
+int max_coresident(int op, int dt, int red, int tma) {
   KernFn fn = op == OP_ALLREDUCE_ONESHOT ? pick_oneshot(dt, red) : pick(op, dt, red);
   int per_sm = 0, dev = 0, sms = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)fn, kThreads, 0) != cudaSuccess) return 0;
+  const size_t smem = dyn_smem(op, tma);
+  if (allow_smem(fn, smem) != cudaSuccess) return 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)fn, kThreads, smem) != cudaSuccess) return 0;
   return per_sm * sms;
 }
 

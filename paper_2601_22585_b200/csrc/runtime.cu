@@ -19,7 +19,7 @@
 namespace hetccl {
 cudaError_t launch_collective(const OpArgs& a, int nlocal, int dt, int red, bool cooperative, cudaStream_t s);
 cudaError_t launch_copy(const void* src, void* dst, size_t n, int es, cudaStream_t s);
-int max_coresident(int op, int dt, int red);
+int max_coresident(int op, int dt, int red, int tma);
 cudaError_t nvls_allreduce(NvlsState* s, const void* send, void* recv, size_t count, int dt, unsigned long long* err,
                            long long timeout_ns, cudaStream_t st);
 }  // namespace hetccl
@@ -46,6 +46,7 @@ struct hetcclComm {
   int trace_iters = 0;                    // HETCCL_TRACE_ITERS: per-iteration timestamps of the last op
   int ws = 0;                             // HETCCL_WS: 0 plain pipeline, k in 2..4 warp-specialised (spacing k)
   int direct = 1;                         // HETCCL_DIRECT: write All-Reduce results straight into peers' recv
+  int tma = 1;                            // HETCCL_TMA: movers stage sources through the TMA shared-memory ring
   int nslots = 8;                         // HETCCL_NSLOTS: scratch ring depth
   size_t os_bytes = 0;                    // HETCCL_ONESHOT_KB: one-shot AR up to this many bytes per rank
   size_t os_chan = 0;                     // bytes per (buffer, sender, channel): each channel owns its region
@@ -122,7 +123,7 @@ size_t alloc_bytes_for(const hetcclComm* c) {
 }
 
 void read_env(hetcclComm* c) {
-  c->nch_max = (int)std::max(1L, std::min((long)kMaxChannels, env_long("HETCCL_NCHANNELS", kMaxChannels)));
+  c->nch_max = (int)std::max(1L, std::min((long)kMaxChannels, env_long("HETCCL_NCHANNELS", kDefaultChannels)));
   // scratch slot: HETCCL_SLOT_KB, else sized from this map so every op's default tile fits
   const long slot_kb = env_long("HETCCL_SLOT_KB", 0);
   c->slot_bytes = slot_kb > 0 ? (size_t)std::max(64L, slot_kb) * 1024
@@ -132,6 +133,7 @@ void read_env(hetcclComm* c) {
   c->trace_iters = (int)std::max(0L, std::min(4096L, env_long("HETCCL_TRACE_ITERS", 0)));
   c->ws = (int)env_long("HETCCL_WS", 0);
   c->direct = env_long("HETCCL_DIRECT", 1) != 0;
+  c->tma = env_long("HETCCL_TMA", 1) != 0;
   if (c->ws == 1 || c->ws < 0) c->ws = 0;
   if (c->ws > 4) c->ws = 4;
   c->nslots = (int)std::max(2L, std::min((long)kMaxSlots, env_long("HETCCL_NSLOTS", 8)));
@@ -266,7 +268,7 @@ hetcclResult_t run_op(hetcclComm_t c, int op, const void* const* sends, void* co
   }
   int nch_max = c->nch_max;
   if (c->kind == KIND_MUX) {
-    int cap = max_coresident(oneshot ? OP_ALLREDUCE_ONESHOT : op, dt, red);
+    int cap = max_coresident(oneshot ? OP_ALLREDUCE_ONESHOT : op, dt, red, c->tma);
     if (cap < nlocal) return fail(c, hetcclInternalError, "device cannot co-schedule %d ranks", nlocal);
     nch_max = std::min(nch_max, cap / nlocal);
   }
@@ -304,6 +306,7 @@ hetcclResult_t run_op(hetcclComm_t c, int op, const void* const* sends, void* co
   a.timeout_ns = c->timeout_ns;
   a.ws = c->ws;
   a.nslots = c->nslots;
+  a.tma = c->tma;
   // direct recv mode: in a rank-multiplexed comm every rank's recv buffer is a local pointer; with one
   // rank per GPU, when recvbuf lies in a connected symmetric buffer (hetccl_mem_*), at the same offset in
   // every peer's copy
@@ -328,8 +331,10 @@ hetcclResult_t run_op(hetcclComm_t c, int op, const void* const* sends, void* co
   // those): a deviation for NVSwitch (R20). HETCCL_FLAT_AG: 1 always, 0 never, unset = messages of
   // at most HETCCL_FLAT_AG_MAX_KB (32768) per rank, where one tile per channel walks the stages serially
   // and dropping one stage pays (q16, 2+2: 8 MiB +19%, 16 MiB +11%, 32 MiB +4%; 64 MiB and up ±0..2%).
+  // Rank-multiplexed comms take it at every size (stage D re-read y from HBM to forward it; r02k: 4+4 mux
+  // 430 -> 466 GB/s).
   const long flat_env = env_long("HETCCL_FLAT_AG", -1);
-  const bool flat_band = count * (size_t)es <= (size_t)env_long("HETCCL_FLAT_AG_MAX_KB", 32768) * 1024;
+  const bool flat_band = c->kind == KIND_MUX || count * (size_t)es <= (size_t)env_long("HETCCL_FLAT_AG_MAX_KB", 32768) * 1024;
   if (a.direct && a.final_stage == 4 && c->topo.D > 1 && (flat_env == 1 || (flat_env < 0 && flat_band))) {
     a.flat_ag = 1;
     a.active &= ~(1u << 3);
@@ -581,14 +586,17 @@ hetcclResult_t hetccl_comm_init_mux(hetcclComm_t* comm, int nranks, const int* r
   c->kind = KIND_MUX;
   c->device = cuda_device;
   DevGuard g(cuda_device);
-  {  // all ranks' CTAs must be co-resident (one per SM): channels per rank <= SMs / nranks
+  {  // all ranks' CTAs must be co-resident: channels per rank <= SMs x CTAs per SM / nranks (every SM slot
+     // unless HETCCL_NCHANNELS caps it)
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cuda_device);
+    c->nch_max = (int)std::max(1L, std::min((long)kMaxChannels, env_long("HETCCL_NCHANNELS", kMaxChannels)));
     c->nch_max = std::max(1, std::min(c->nch_max, sms * kCtasPerSm / nranks));
     // few channels per rank: 1 MiB tiles amortise the per-iteration protocol (measured 262 -> 356 GB/s)
     c->tile_base = (size_t)1 << 20;
+    const int nch = c->nch_max;
     read_env(c);  // re-derive the slot from the larger tile
-    c->nch_max = std::max(1, std::min(c->nch_max, sms * kCtasPerSm / nranks));
+    c->nch_max = nch;
     set_os_layout(c);
     c->alloc_bytes = alloc_bytes_for(c);
   }

@@ -296,3 +296,17 @@ def test_broadcast_allgather_alltoall_labels():
     ys = oracle.all_to_all(xs, "int32")
     for i in range(n):
         np.testing.assert_array_equal(ys[i], np.concatenate([xs[j][2 * i:2 * i + 2] for j in range(n)]))
+
+
+@pytest.mark.parametrize("dt,op", [("bf16", "sum"), ("f32", "sum"), ("int32", "max"), ("f16", "min")])
+@pytest.mark.parametrize("m", [[0, 0, 0, 0, 1, 1, 1, 1], [0, 1, 2, 2], [1, 0, 1, 0, 2, 2]])
+def test_threaded_oracle_splits_elements_only(dt, op, m):
+    """the T-thread oracle splits elements only, so its Y is bit-identical to the serial one
+    (ragged per-thread ranges, more threads than some ranges)."""
+    n, count = len(m), 100_003
+    kind = "bits" if dt == "int32" else "normal"
+    xs = [synth.make(kind, 41, r, count, dt) for r in range(n)]
+    want = oracle.allreduce(xs, m, dt, op)
+    for T in (1, 3, 7, 16):
+        got = oracle.allreduce_threaded(xs, m, dt, op, threads=T)
+        assert np.array_equal(got.view(np.uint8), want.view(np.uint8)), f"T={T}"

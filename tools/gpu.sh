@@ -52,7 +52,7 @@ for s in $STEPS; do
       for v in ${LIBS:-default}; do
         for e in ${ENVS:-NONE=1}; do
           lib=libhetccl.so; [ "$v" = default ] || lib=libhetccl_$v.so
-          env $e HETCCL_LIB=$lib timeout 300 python bench.py --no-cpu-baseline --steps ${ABSTEPS:-20} > $O/ab_${v}_${e}.json 2> $O/ab_${v}_${e}.err
+          env ${e//,/ } HETCCL_LIB=$lib timeout 300 python bench.py --no-cpu-baseline --steps ${ABSTEPS:-20} ${BARGS} > $O/ab_${v}_${e}.json 2> $O/ab_${v}_${e}.err
           echo "$v $e $(python -c "import json,sys; d=json.load(open('$O/ab_${v}_${e}.json')); print(d['value'], d['roofline']['frac'])" 2>&1)" >> $O/mux_ab.txt
         done
       done ;;
