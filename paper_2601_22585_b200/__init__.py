@@ -228,14 +228,15 @@ def nvls_buffer(comm, numel, dtype, device):
 
 def hetccl_comm_get_trace(comm):
     """Per-iteration timestamps of the last op (HETCCL_TRACE_ITERS at comm creation): numpy uint64
-    array [local ranks, channels, iterations, 8] (wait start, work start, work end, fenced, end of logical
-    stages 0..3 on thread 0 — 0 where the stage did not run), or None."""
+    array [local ranks, channels, iterations, 10] (wait start, work start, work end, fenced, end of logical
+    stages 0..3 on thread 0 — 0 where the stage did not run; iteration 0 also holds the kernel entry and exit
+    stamps in words 8 and 9), or None."""
     import numpy as np
     shape = (ctypes.c_int * 3)()
     _check(lib().hetccl_comm_get_trace(comm, None, 0, shape), comm)
     if shape[0] == 0:
         return None
-    out = np.zeros((shape[0], shape[1], shape[2], 8), np.uint64)
+    out = np.zeros((shape[0], shape[1], shape[2], 10), np.uint64)
     _check(lib().hetccl_comm_get_trace(comm, out.ctypes.data, out.nbytes, shape), comm)
     return out
 

@@ -31,7 +31,8 @@ constexpr int kMaxSlots = 16;      // cap on the scratch ring depth per channel 
 #endif
 constexpr int kThreads = HETCCL_THREADS;  // threads per CTA (kCtasPerSm CTAs per SM)
 constexpr int kMaxStages = 5;      // pipeline positions of the deepest op (All-Reduce)
-constexpr int kTraceWords = 8;     // per traced iteration: poll start, GO, DONE, fenced, end of stages 0..3
+constexpr int kTraceWords = 10;    // per traced iteration: poll start, GO, DONE, fenced, end of stages 0..3;
+                                   // iteration 0 also: kernel entry, kernel exit (after the final wait)
 
 // counters (per rank, per channel); C_ACK counts tiles a sender has fully consumed
 // C_OS / C_OSACK belong to the one-shot small-message All-Reduce (k_allreduce_oneshot).
@@ -124,6 +125,8 @@ struct OpArgs {
   int pull;                     // 1 (with direct): every rank's send buffer is addressable (peer_send): the domain
   const void* peer_send[kMaxRanks];  // fold reads peers' x directly, stage A and the s1 staging vanish
   int tma;                      // 1: the movers stage their sources through the TMA ring (dynamic shared memory)
+  int l2hint;                   // 1: L2 policies in the TMA movers (evict_first streams, evict_last + discard partials)
+  int spacing;                  // plain pipeline (ws == 0): positions between consecutive stages (1 = adjacent)
 };
 
 // ---- host plan (plan.cpp) ----

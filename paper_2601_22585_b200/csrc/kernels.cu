@@ -170,8 +170,11 @@ constexpr int kMaxList = kMaxRanks + 2;
 struct PtrList {
   const void* p[kMaxList];
   int n;
-  __device__ PtrList() : n(0) {}
+  uint32_t keep;  // L2 hints (HETCCL_L2HINT): destinations -> store evict_last (read back soon: the cross
+                  // partials); sources -> dead after this read (discard their L2 lines, no write-back)
+  __device__ PtrList() : n(0), keep(0) {}
   __device__ void add(const void* q) { p[n++] = q; }
+  __device__ void add_keep(const void* q) { keep |= 1u << n; p[n++] = q; }
 };
 
 __device__ __forceinline__ bool all_aligned16(const PtrList& a, const PtrList& b) {
@@ -293,13 +296,41 @@ __device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, uint32_t 
                "l"(gsrc), "r"(bytes), "r"(smem_addr(b))
                : "memory");
 }
+__device__ __forceinline__ void bulk_g2s_hint(void* sdst, const void* gsrc, uint32_t bytes, uint64_t* b, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_addr(sdst)),
+      "l"(gsrc), "r"(bytes), "r"(smem_addr(b)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void st_v4_hint(void* p, const uint4& v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void discard_l2(const void* p) {
+  asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
+}
+__shared__ int g_l2hint;  // OpArgs::l2hint of the running op
+__shared__ uint32_t g_keep_dst, g_dead_ops;  // the current call's hint masks (destinations / operands)
 __device__ __forceinline__ void data_bar() { asm volatile("bar.sync 1, %0;" ::"r"(g_dnth) : "memory"); }
 
 // thread 0 at the start of a pipeline kernel, before its first __syncthreads (data warps: all warps, or
 // all but the sync warp in the warp-specialised mode)
-__device__ __forceinline__ void tma_init(int enable, int data_warps) {
+__device__ __forceinline__ void tma_init(int enable, int data_warps, int l2hint) {
   if (threadIdx.x == 0) {
     g_tma = HETCCL_TMA && enable;
+    g_l2hint = l2hint;
     g_seq = 0;
     if (g_tma) {
       for (int s = 0; s < kTmaStages; s++) {
@@ -334,31 +365,40 @@ __device__ __noinline__ void tma_stream(int ni, int D, int kpos, int nd, uint32_
   const uint32_t cv = min((uint32_t)(kTmaStageBytes / (nops * 16)) / kTmaAlignV * kTmaAlignV, (uint32_t)(kTmaMaxVpt * nth));
   const uint32_t chb = cv * 16;
   const uint32_t nchunks = (nv + cv - 1) / cv;
-  const uint32_t ring = smem_addr(g_ring), full = smem_addr(g_full), empty = smem_addr(g_empty);
-  if (tid == 0) {
-    for (uint32_t c = 0; c < nchunks && c < (uint32_t)kTmaStages - 1; c++) {
-      const unsigned g = seq0 + c, st = g % kTmaStages, u = g / kTmaStages;
-      if (u > 0) mbar_wait(&g_empty[st], (u - 1) & 1u);
-      const uint32_t bytes = min(cv, nv - c * cv) * 16;
-      mbar_arrive_expect_tx(&g_full[st], bytes * (uint32_t)nops);
-      for (int j = 0; j < nops; j++) bulk_g2s(g_ring + st * kTmaStageBytes + j * chb, g_ops[j] + (size_t)c * chb, bytes, &g_full[st]);
+  // L2 policy (HETCCL_L2HINT): every operand and result is touched once, so loads and stores stream with
+  // evict_first; the cross partials (keep-masked destinations) are stored evict_last so they are still in L2
+  // when their owner's next stage reads them, and after that read (dead-masked operands) their lines are
+  // discarded — never written back to HBM.
+  // HETCCL_L2HINT bits: 1 evict_first on streamed loads/stores, 2 evict_last on kept stores, 4 discard dead operands
+  const int hint = g_l2hint & 3;
+  const uint32_t keep = (g_l2hint & 2) ? g_keep_dst : 0u, dead = (g_l2hint & 4) ? g_dead_ops : 0u;
+  const uint64_t pol_first = policy_evict_first(), pol_last = policy_evict_last();
+  auto issue = [&](uint32_t cn) {
+    const unsigned g = seq0 + cn, st = g % kTmaStages, u = g / kTmaStages;
+    if (u > 0) mbar_wait(&g_empty[st], (u - 1) & 1u);  // every data warp is done with the stage's last use
+    const uint32_t bytes = min(cv, nv - cn * cv) * 16;
+    mbar_arrive_expect_tx(&g_full[st], bytes * (uint32_t)nops);
+    for (int j = 0; j < nops; j++) {
+      if (hint & 1) bulk_g2s_hint(g_ring + st * kTmaStageBytes + j * chb, g_ops[j] + (size_t)cn * chb, bytes, &g_full[st], pol_first);
+      else bulk_g2s(g_ring + st * kTmaStageBytes + j * chb, g_ops[j] + (size_t)cn * chb, bytes, &g_full[st]);
     }
-  }
-  (void)ring;
-  (void)full;
-  (void)empty;
+  };
+  if (tid == 0)
+    for (uint32_t c = 0; c < nchunks && c < (uint32_t)kTmaStages - 1; c++) issue(c);
   const int lane = threadIdx.x & 31;
   for (uint32_t c = 0; c < nchunks; c++) {
-    if (tid == 0 && c + kTmaStages - 1 < nchunks) {
-      const uint32_t cn = c + kTmaStages - 1;
-      const unsigned g = seq0 + cn, st = g % kTmaStages, u = g / kTmaStages;
-      if (u > 0) mbar_wait(&g_empty[st], (u - 1) & 1u);  // every data warp is done with the stage's last use
-      const uint32_t bytes = min(cv, nv - cn * cv) * 16;
-      mbar_arrive_expect_tx(&g_full[st], bytes * (uint32_t)nops);
-      for (int j = 0; j < nops; j++) bulk_g2s(g_ring + st * kTmaStageBytes + j * chb, g_ops[j] + (size_t)cn * chb, bytes, &g_full[st]);
-    }
+    if (tid == 0 && c + kTmaStages - 1 < nchunks) issue(c + kTmaStages - 1);
     const unsigned g = seq0 + c, st = g % kTmaStages;
     mbar_wait(&g_full[st], (g / kTmaStages) & 1u);
+    if (dead) {  // the chunk of every dead operand is in shared memory: drop its whole 128-byte lines from L2
+      const uint32_t bytes = min(cv, nv - c * cv) * 16;
+      for (int j = 0; j < nops; j++) {
+        if (!((dead >> j) & 1u)) continue;
+        const uintptr_t a0 = (uintptr_t)(g_ops[j] + (size_t)c * chb), a1 = a0 + bytes;
+        for (uintptr_t l = (a0 + 127) / 128 * 128 + (uintptr_t)tid * 128; l + 128 <= a1; l += (uintptr_t)nth * 128)
+          discard_l2((const void*)l);
+      }
+    }
     const unsigned char* sb = g_ring + st * kTmaStageBytes;
     const uint32_t lim = min(cv, nv - c * cv);
     for (uint32_t idx = tid; idx < lim; idx += nth) {
@@ -392,7 +432,18 @@ __device__ __noinline__ void tma_stream(int ni, int D, int kpos, int nd, uint32_
         for (int e = 0; e < V; e++) Vec<S>::set(o, e, TR::narrow(acc[e]));
       }
       const size_t off = ((size_t)c * cv + idx) * 16;
-      for (int d = 0; d < nd; d++) st_v4(g_dst[d] + off, o);
+      if (hint == 3) {
+        for (int d = 0; d < nd; d++) st_v4_hint(g_dst[d] + off, o, ((keep >> d) & 1u) ? pol_last : pol_first);
+      } else if (hint == 2) {
+        for (int d = 0; d < nd; d++) {
+          if ((keep >> d) & 1u) st_v4_hint(g_dst[d] + off, o, pol_last);
+          else st_v4(g_dst[d] + off, o);
+        }
+      } else if (hint == 1) {
+        for (int d = 0; d < nd; d++) st_v4_hint(g_dst[d] + off, o, pol_first);
+      } else {
+        for (int d = 0; d < nd; d++) st_v4(g_dst[d] + off, o);
+      }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&g_empty[st]);  // this warp is done with stage st
@@ -415,6 +466,15 @@ __device__ __forceinline__ void tma_move(const PtrList& inner, int kpos, const P
   const unsigned seq0 = *(volatile unsigned*)&g_seq;  // read before the 2nd barrier: no thread can move it on yet
   if (tid < nops) g_ops[tid] = (const char*)(tid < ni ? inner.p[tid] : outer.p[tid - ni < kpos ? tid - ni : tid - ni + 1]);
   if (tid < nd) g_dst[tid] = (char*)dsts.p[tid];
+  if (tid == 0) {
+    g_keep_dst = dsts.keep;
+    // dead operands in load order: inner bits as is, outer bits (q != kpos) after them
+    uint32_t dm = inner.keep;
+    if (MODE == 2)
+      for (int q = 0; q < D; q++)
+        if (q != kpos && ((outer.keep >> q) & 1u)) dm |= 1u << (ni + (q < kpos ? q : q - 1));
+    g_dead_ops = dm;
+  }
   data_bar();
   tma_stream<T, OP, MODE>(ni, D, kpos, nd, (uint32_t)nv, seq0);
 }
@@ -987,6 +1047,7 @@ struct Pipe {
 
 template <class Op>
 __device__ __forceinline__ void run_pipeline(const OpArgs& a, Op& op, int me, int ch) {
+  const unsigned long long t_entry = globaltimer();
   __shared__ PipeShared ps;
   Pipe<Op> P{a, op, ps, a.rp[me]};
   P.me = me;
@@ -996,7 +1057,7 @@ __device__ __forceinline__ void run_pipeline(const OpArgs& a, Op& op, int me, in
   P.F = chan_flags(a, me, ch);
   uint64_t* B = chan_base(a, me, ch);
   const bool ws = a.ws >= 2;
-  P.SP = ws ? a.ws : 1;
+  P.SP = ws ? a.ws : (a.spacing > 1 ? a.spacing : 1);  // plain mode: consumer positions SP apart (slack)
   P.np = 0;
   for (int p = 0; p < 4 * kMaxStages; p++) P.stage_at[p] = -1;
 #pragma unroll
@@ -1005,7 +1066,7 @@ __device__ __forceinline__ void run_pipeline(const OpArgs& a, Op& op, int me, in
   P.npos = P.SP * (P.np - 1) + 1;
   if (threadIdx.x < kCounters * kMaxRanks)
     ps.base[threadIdx.x / kMaxRanks][threadIdx.x % kMaxRanks] = B[threadIdx.x / kMaxRanks * kLineWords + threadIdx.x % kMaxRanks];
-  tma_init(a.tma, (a.ws >= 2 ? (int)blockDim.x - 32 : (int)blockDim.x) / 32);
+  tma_init(a.tma, (a.ws >= 2 ? (int)blockDim.x - 32 : (int)blockDim.x) / 32, a.l2hint);
   if (threadIdx.x == 0) {
     ps.tiles0 = B[kCounters * kLineWords];
     ps.abort_ = 0;
@@ -1116,6 +1177,10 @@ __device__ __forceinline__ void run_pipeline(const OpArgs& a, Op& op, int me, in
     }
   }
   __syncthreads();
+  if (trc && threadIdx.x == 0) {
+    trc[8] = t_entry;
+    trc[9] = globaltimer();
+  }
   // ---- exit: advance this rank's cumulative targets by the tiles this launch processed ----
   if (!ps.abort_ && threadIdx.x < kMaxRanks) {
     const int p = threadIdx.x;
@@ -1204,7 +1269,7 @@ struct ArOp {
           } else {
             const int o = owner_of(tp, q, sg);
             const int dq = tp.dom_size[q];
-            dst.add(slot_ptr<T>(a, o, ch, slot) + s2_off(dq) + (size_t)k * (TL / dq) + (c0 - region_lo(g, o)));
+            dst.add_keep(slot_ptr<T>(a, o, ch, slot) + s2_off(dq) + (size_t)k * (TL / dq) + (c0 - region_lo(g, o)));
           }
           cta_fold<T, OP>(src, dst, c1 - c0);
         }
@@ -1215,7 +1280,10 @@ struct ArOp {
         if (c1 <= c0) continue;
         PtrList inner, outer, dst;
         for (int i = 0; i < d; i++) inner.add(i == j ? (const void*)(x + tb + c0) : dsrc(i, slot, tb, c0, r0));
-        for (int q = 0; q < D; q++) outer.add(q == k ? nullptr : (const void*)(my_s2 + (size_t)q * Rk + (c0 - r0)));
+        for (int q = 0; q < D; q++) {
+          if (q == k) outer.add(nullptr);
+          else outer.add_keep(my_s2 + (size_t)q * Rk + (c0 - r0));  // dead after this read
+        }
         dst.add(y + tb + c0);
         for (int q = 0; q < D; q++) {
           if (q == k) continue;
@@ -1353,7 +1421,7 @@ struct RsOp {
                          : (const void*)(mine + (size_t)cidx(i, j) * RG + TL + (size_t)ro * Pc));
         const int dr = tp.dom_size[tp.rank_dom[r]];
         const size_t RGr = TL + (size_t)(n - dr) * (TL / dr);
-        dst.add(slot_ptr<T>(a, r, ch, slot) + (size_t)(dr - 1) * RGr + (size_t)k * TL + pj0);
+        dst.add_keep(slot_ptr<T>(a, r, ch, slot) + (size_t)(dr - 1) * RGr + (size_t)k * TL + pj0);
         cta_fold<T, OP>(src, dst, pj1 - pj0);
         ro++;
       }
@@ -1361,8 +1429,10 @@ struct RsOp {
       PtrList inner, outer, dst;
       for (int i = 0; i < d; i++)
         inner.add(i == j ? (const void*)(x + (size_t)me * R + tb) : (const void*)(mine + (size_t)cidx(i, j) * RG));
-      for (int q = 0; q < D; q++)
-        outer.add(q == k ? nullptr : (const void*)(mine + (size_t)(d - 1) * RG + (size_t)q * TL));
+      for (int q = 0; q < D; q++) {
+        if (q == k) outer.add(nullptr);
+        else outer.add_keep(mine + (size_t)(d - 1) * RG + (size_t)q * TL);  // dead after this read
+      }
       dst.add(y + tb);
       cta_fold_hier<T, OP>(inner, k, outer, dst, len);
     }

@@ -307,6 +307,8 @@ hetcclResult_t run_op(hetcclComm_t c, int op, const void* const* sends, void* co
   a.ws = c->ws;
   a.nslots = c->nslots;
   a.tma = c->tma;
+  a.spacing = (int)std::max(1L, std::min(4L, env_long("HETCCL_SPACING", 1)));
+  a.l2hint = (int)env_long("HETCCL_L2HINT", 1);  // evict_first streams (r02n: +4%; partial keep/discard bits 2/4 lose)
   // direct recv mode: in a rank-multiplexed comm every rank's recv buffer is a local pointer; with one
   // rank per GPU, when recvbuf lies in a connected symmetric buffer (hetccl_mem_*), at the same offset in
   // every peer's copy
@@ -383,7 +385,8 @@ hetcclResult_t run_op(hetcclComm_t c, int op, const void* const* sends, void* co
   {  // the ring must be deeper than the pipeline (plus the one-iteration release lag of the WS mode)
     int na = 0;
     for (int s = 0; s < kMaxStages; s++) na += (a.active >> s) & 1;
-    const int npos = (c->ws >= 2 ? c->ws : 1) * (na - 1) + 1 + (c->ws >= 2 ? 1 : 0);
+    const int sp = c->ws >= 2 ? c->ws : std::max(1, a.spacing);
+    const int npos = sp * (na - 1) + 1 + (c->ws >= 2 ? 1 : 0);
     if (c->nslots <= npos)
       return fail(c, hetcclInvalidUsage, "HETCCL_NSLOTS=%d must exceed the pipeline depth %d", c->nslots, npos);
   }

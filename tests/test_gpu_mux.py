@@ -127,11 +127,14 @@ def test_trace_stamps_monotone(monkeypatch):
         ys = [torch.empty_like(x) for x in xs]
         hc.mux_allreduce(xs, ys, comm)
         tr = hc.hetccl_comm_get_trace(comm)
-        assert tr is not None and tr.shape[0] == 4 and tr.shape[3] == 8
+        assert tr is not None and tr.shape[0] == 4 and tr.shape[3] == 10
         used = tr[..., 0] > 0
         assert used.any()
         for k in range(3):
             assert np.all(tr[..., k + 1][used] >= tr[..., k][used])
+        # kernel entry <= first poll, last fence <= kernel exit (iteration 0 row, words 8 and 9)
+        ch = used[..., 0]
+        assert np.all(tr[..., 0, 8][ch] <= tr[..., 0, 0][ch]) and np.all(tr[..., 0, 9][ch] >= tr[..., 0, 3][ch])
     finally:
         hc.hetccl_comm_destroy(comm)
 

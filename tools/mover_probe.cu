@@ -180,12 +180,86 @@ __device__ void mv_tma(const Args& a, size_t off, size_t nv, unsigned char* ring
   *(volatile unsigned*)&s_seq = seq0 + (unsigned)nch;
 }
 
+// ---------------------------------------------------------------- tma2: the library's mover (full/empty
+// mbarriers, no CTA barrier per chunk, evict_first hints); S2G=1 stores results with bulk copies from shared
+__shared__ __align__(8) uint64_t s_empty[16];
+__device__ __forceinline__ void mwait(uint64_t* b, uint32_t par) {
+  uint32_t ok = 0;
+  while (!ok)
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(ok)
+                 : "r"(sa(b)), "r"(par)
+                 : "memory");
+}
+template <int S2G>
+__device__ void mv_tma2(const Args& a, size_t off, size_t nv_, unsigned char* ring) {
+  const int tid = threadIdx.x, nth = blockDim.x, NST = a.NST, lane = tid & 31;
+  const uint32_t nv = (uint32_t)nv_;
+  const uint32_t cv = min((uint32_t)(a.SB / (a.K * 16)) / 8 * 8, (uint32_t)(4 * nth));
+  const uint32_t chb = cv * 16, nch = (nv + cv - 1) / cv;
+  const unsigned seq0 = *(volatile unsigned*)&s_seq;
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  auto issue = [&](uint32_t cn) {
+    const unsigned g = seq0 + cn, st = g % NST, u = g / NST;
+    if (u > 0) mwait(&s_empty[st], (u - 1) & 1u);
+    if (S2G && u > 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    const uint32_t bytes = min(cv, nv - cn * cv) * 16;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(&s_full[st])), "r"(bytes * a.K) : "memory");
+    for (int k = 0; k < a.K; k++)
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+              sa(ring + (size_t)st * a.SB + (size_t)k * chb)),
+          "l"(a.src[k] + off + (size_t)cn * chb), "r"(bytes), "r"(sa(&s_full[st])), "l"(pol)
+          : "memory");
+  };
+  if (tid == 0)
+    for (uint32_t c = 0; c < nch && c < (uint32_t)NST - 1; c++) issue(c);
+  for (uint32_t c = 0; c < nch; c++) {
+    if (tid == 0 && c + NST - 1 < nch) issue(c + NST - 1);
+    const unsigned g = seq0 + c, st = g % NST;
+    mwait(&s_full[st], (g / NST) & 1u);
+    unsigned char* sb = ring + (size_t)st * a.SB;
+    const uint32_t lim = min(cv, nv - c * cv);
+    for (uint32_t idx = tid; idx < lim; idx += nth) {
+      float acc[8];
+      acc_add(acc, *(const uint4*)(sb + idx * 16), true);
+#pragma unroll 1
+      for (int k = 1; k < a.K; k++) acc_add(acc, *(const uint4*)(sb + k * chb + idx * 16), false);
+      const uint4 o = a.K == 1 ? *(const uint4*)(sb + idx * 16) : pack(acc);
+      if (S2G) *(uint4*)(sb + idx * 16) = o;
+      else
+        for (int m = 0; m < a.M; m++)
+          asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(a.dst[m] + off + ((size_t)c * cv + idx) * 16),
+                       "r"(o.x), "r"(o.y), "r"(o.z), "r"(o.w), "l"(pol)
+                       : "memory");
+    }
+    if (S2G) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncthreads();  // every result of the chunk is in shared memory
+      if (tid == 0) {
+        for (int m = 0; m < a.M; m++)
+          asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(
+                           a.dst[m] + off + (size_t)c * chb),
+                       "r"(sa(sb)), "r"(lim * 16), "l"(pol)
+                       : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+    }
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sa(&s_empty[st])) : "memory");
+  }
+  if (S2G && tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  *(volatile unsigned*)&s_seq = seq0 + nch;
+}
+
 template <int IMPL, int U>
 __global__ void __launch_bounds__(128) k_probe(const __grid_constant__ Args a) {
   extern __shared__ __align__(128) unsigned char dyn[];
-  if (IMPL == 2) {
+  if (IMPL >= 2) {
     if (threadIdx.x == 0) {
       for (int s = 0; s < a.NST; s++) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa(&s_full[s])));
+      for (int s = 0; s < a.NST; s++) asm volatile("mbarrier.init.shared::cta.b64 [%0], 4;" ::"r"(sa(&s_empty[s])));
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
       s_seq = 0;
     }
@@ -196,7 +270,9 @@ __global__ void __launch_bounds__(128) k_probe(const __grid_constant__ Args a) {
     const size_t off = b * a.BLK, nv = a.BLK / 16;
     if (IMPL == 0) mv_ldg<U>(a, off, nv);
     else if (IMPL == 1) mv_lgsts<U>(a, off, nv, (uint4*)dyn);
-    else mv_tma(a, off, nv, dyn);
+    else if (IMPL == 2) mv_tma(a, off, nv, dyn);
+    else if (IMPL == 3) mv_tma2<0>(a, off, nv, dyn);
+    else mv_tma2<1>(a, off, nv, dyn);
   }
 }
 
@@ -222,14 +298,14 @@ int main(int argc, char** argv) {
   const Shape shapes[] = {{5, 8}, {5, 5}, {4, 1}, {1, 3}, {1, 1}};
   struct Cfg { const char* name; int impl, U, PF, NST, SB, VPT, ctas_per_sm; };
   std::vector<Cfg> cfgs = {
-      {"ldg_u4", 0, 4, 0, 0, 0, 0, 2},        {"lgsts_u4", 1, 4, 0, 0, 0, 0, 2},
-      {"lgsts_u4_pf2", 1, 4, 2, 0, 0, 0, 2},  {"tma_4x24k", 2, 0, 0, 4, 24576, 4, 2},
-      {"tma_3x32k", 2, 0, 0, 3, 32768, 4, 2}, {"tma_4x24k_pf4", 2, 0, 4, 4, 24576, 4, 2},
-      {"tma_3x32k_pf4", 2, 0, 4, 3, 32768, 4, 2}, {"tma_4x48k", 2, 0, 0, 4, 49152, 8, 1},
-      {"tma_6x32k", 2, 0, 0, 6, 32768, 8, 1},  {"tma_8x12k", 2, 0, 0, 8, 12288, 4, 2},
-      {"tma_3x16k_4cta", 2, 0, 0, 3, 16384, 4, 4}, {"tma_3x16k_4cta_pf4", 2, 0, 4, 3, 16384, 4, 4},
+      {"lgsts_u4_pf2", 1, 4, 2, 0, 0, 0, 2},     {"tma2_3x16k_c4", 3, 0, 0, 3, 16384, 4, 4},
+      {"tma2_4x12k_c4", 3, 0, 0, 4, 12288, 4, 4}, {"tma2_2x24k_c4", 3, 0, 0, 2, 24576, 4, 4},
+      {"s2g_3x16k_c4", 4, 0, 0, 3, 16384, 4, 4},  {"s2g_4x12k_c4", 4, 0, 0, 4, 12288, 4, 4},
+      {"tma2_3x24k_c3", 3, 0, 0, 3, 24576, 4, 3}, {"s2g_3x24k_c3", 4, 0, 0, 3, 24576, 4, 3},
+      {"tma2_4x24k_c2", 3, 0, 0, 4, 24576, 4, 2}, {"s2g_4x24k_c2", 4, 0, 0, 4, 24576, 4, 2},
+      {"tma2_3x8k_c6", 3, 0, 0, 3, 8192, 4, 6},
   };
-  const size_t blks[] = {128 << 10, 1 << 20};
+  const size_t blks[] = {128 << 10};
   for (const Shape& sh : shapes)
     for (size_t BLK : blks)
       for (const Cfg& c : cfgs) {
@@ -246,10 +322,14 @@ int main(int argc, char** argv) {
         a.NST = c.NST;
         a.SB = c.SB;
         a.VPT = c.VPT;
-        size_t smem = c.impl == 1 ? (size_t)sh.K * c.U * 128 * 16 : c.impl == 2 ? (size_t)c.NST * c.SB : 0;
-        void (*fn)(Args) = c.impl == 0 ? k_probe<0, 4> : c.impl == 1 ? k_probe<1, 4> : k_probe<2, 4>;
+        size_t smem = c.impl == 1 ? (size_t)sh.K * c.U * 128 * 16 : c.impl >= 2 ? (size_t)c.NST * c.SB : 0;
+        void (*fn)(Args) = c.impl == 0   ? k_probe<0, 4>
+                           : c.impl == 1 ? k_probe<1, 4>
+                           : c.impl == 2 ? k_probe<2, 4>
+                           : c.impl == 3 ? k_probe<3, 4>
+                                         : k_probe<4, 4>;
         CK(cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        if (c.impl == 2 && (size_t)sh.K * 16 * 128 > (size_t)c.SB) continue;
+        if (c.impl >= 2 && (size_t)sh.K * 16 * 32 > (size_t)c.SB) continue;
         const int grid = 148 * c.ctas_per_sm;
         float best = 1e30f;
         for (int rep = 0; rep < 5; rep++) {

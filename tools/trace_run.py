@@ -27,6 +27,11 @@ def summarize(tr, label):
     work = (tr[..., 2] - tr[..., 1]).astype(np.int64)[used]
     fence = (tr[..., 3] - tr[..., 2]).astype(np.int64)[used]
     nit = used.sum(axis=2)
+    if tr.shape[-1] >= 10:
+        ent, ext = tr[..., 0, 8].astype(np.int64), tr[..., 0, 9].astype(np.int64)
+        e0 = ent[ent > 0].min()
+        print(f"{label}: kernel entry spread {(ent.max() - e0) / 1e3:.1f} us, first poll {(t0 - e0) / 1e3:.1f} us after "
+              f"the first entry, exits {(ext[ext > 0].min() - e0) / 1e3:.1f}..{(ext.max() - e0) / 1e3:.1f} us")
     print(f"{label}: span {(t_end - t0) / 1e3:.1f} us, iterations/channel {nit.min()}..{nit.max()}, "
           f"per iteration mean wait {wait.mean() / 1e3:.2f} us, work {work.mean() / 1e3:.2f} us, "
           f"fence {fence.mean() / 1e3:.2f} us; p90 wait {np.percentile(wait, 90) / 1e3:.2f} "
