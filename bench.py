@@ -129,7 +129,8 @@ class NvlinkCounter:
             pynvml.nvmlInit()
             pr = torch.cuda.get_device_properties(cuda_device)
             bus = f"{pr.pci_domain_id:08X}:{pr.pci_bus_id:02X}:{pr.pci_device_id:02X}.0"
-            self.h = pynvml.nvmlDeviceGetHandleByPciBusId_v2(bus)
+            get = getattr(pynvml, "nvmlDeviceGetHandleByPciBusId_v2", None) or pynvml.nvmlDeviceGetHandleByPciBusId
+            self.h = get(bus)
             self.links = []
             for l in range(pynvml.NVML_NVLINK_MAX_LINKS):
                 try:
@@ -186,7 +187,7 @@ def busbw(nbytes, t_s, n):
     return alg, alg * 2 * (n - 1) / n
 
 
-def oracle_baseline(xs_host, m, recv_dev_list, budget_s=15.0):
+def oracle_baseline(xs_host, m, recv_dev_list, budget_s=15.0, total_count=None):
     """cpu_baseline leg: the oracle as it stands on a bounded sample of the workload, timed twice — on one
     host thread and on every host core (oracle.allreduce_threaded: elements split across threads, same
     per-element fold, bit-identical) — and the GPU result on the same sample compared with it bitwise (the
@@ -195,6 +196,7 @@ def oracle_baseline(xs_host, m, recv_dev_list, budget_s=15.0):
     import torch
     count = xs_host[0].size
     # ~15 ns per element index for 8 ranks single-threaded: bound the sample to the budget
+    total = int(total_count or count)
     sample = int(min(count, max(1 << 16, budget_s / (2e-9 * len(m)))))
     xs = [x[:sample] for x in xs_host]
     t0 = time.perf_counter()
@@ -209,7 +211,7 @@ def oracle_baseline(xs_host, m, recv_dev_list, budget_s=15.0):
     ok = bool(np.array_equal(want, want_t)) and all(
         bool(np.array_equal(y[:sample].cpu().view(torch.int16).numpy().view(np.uint16), want)) for y in recv_dev_list)
     return {"value": round(bust, 3), "unit": "GB/s", "cores": cores, "kind": "oracle",
-            "sample": f"first {sample} of {count} elements per rank, all {len(m)} ranks, one All-Reduce "
+            "sample": f"first {sample} of {total} elements per rank, all {len(m)} ranks, one All-Reduce "
                       f"({dtt:.2f} s on {cores} host threads, elements split across threads; {dt1:.2f} s on 1); "
                       f"busbw convention as value",
             "single_thread": {"value": round(bus1, 3), "unit": "GB/s", "cores": 1},
@@ -441,7 +443,8 @@ def run_dist(args):
         # the oracle on a bounded sample: every rank's first elements regenerated from the generator; checked
         # bitwise against this rank's GPU result on the same elements
         ns = min(count, 1 << 22)
-        cpu = oracle_baseline([synth.normal(SEED, r, ns, "bf16") for r in range(world)], m, [recv[:ns]])
+        cpu = oracle_baseline([synth.normal(SEED, r, ns, "bf16") for r in range(world)], m, [recv[:ns]],
+                              total_count=count)
     dist.barrier()
     hc.hetccl_comm_destroy(comm)
     if rank == 0:

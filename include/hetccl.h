@@ -118,15 +118,19 @@ HETCCL_API hetcclResult_t hetccl_comm_info(hetcclComm_t comm, int* rank, int* nr
  * NVLS mode (opt-in). With HETCCL_NVLS=1 in the environment of
  * hetccl_comm_init_all, and every domain of the same size d >= 2 on devices with multicast support,
  * each domain gets an NVLink SHARP multicast object and hetccl_allreduce (bf16/fp16/fp32 sum, 16-byte
- * aligned buffers) runs its intra-domain reduce-scatter inside the switch (multimem.ld_reduce, fp32
- * accumulation) and its intra-domain all-gather as one multicast store (multimem.st); the cross-domain
- * exchange and fold stay P2P in ascending domain order. The switch's summation order is not R3's, so
- * results are within the R7 gate but not bitwise those of the oracle (R21). Other dtypes,
- * ops and unaligned buffers keep the P2P path.
+ * aligned buffers) runs its intra-domain reduce-scatter inside the switch (multimem.ld_reduce) and its
+ * intra-domain all-gather as one multicast store (multimem.st); the cross-domain exchange and fold stay
+ * P2P in ascending domain order. 16-bit inputs are staged in fp32 (HETCCL_NVLS_WIDE=1, the default: the
+ * switch's fp32 adds are round-to-nearest-even, its 16-bit ones are not) and each partial is narrowed
+ * once, so results meet the R7 gate (elementwise 1e-2 * sum|x|, normwise 1e-2); the switch's summation
+ * order is not R3's, so they are not bitwise those of the oracle (R21). Other dtypes, ops and
+ * unaligned buffers keep the P2P path.
  *   enabled : 1 if this comm runs All-Reduce in NVLS mode, else 0 (hetccl_get_last_error says why).
  *   buffer  : this rank's view of its multicast-bound buffer (device memory owned by the comm, valid
- *             until hetccl_comm_destroy), or NULL. An in-place All-Reduce on it (sendbuf == recvbuf ==
- *             buffer, count * size a multiple of 16 bytes, at most *bytes) skips the copies in and out.
+ *             until hetccl_comm_destroy), or NULL. An in-place f32 All-Reduce on it (sendbuf == recvbuf ==
+ *             buffer, count * size a multiple of 16 bytes, at most *bytes) skips the copies in and out;
+ *             a 16-bit All-Reduce whose buffers overlap it is hetcclInvalidArgument while staging wide
+ *             (the buffer holds the fp32 staging copy).
  *   bytes   : the buffer's usable size (the chunk size, HETCCL_NVLS_MB rounded to the multicast
  *             granularity), or 0.
  * Any output pointer may be NULL. hetcclInvalidArgument on a null comm.

@@ -24,7 +24,8 @@ constexpr int kMaxRanks = 16;      // == HETCCL_MAX_RANKS (one flag line = 16 se
 #endif
 constexpr int kCtasPerSm = HETCCL_CTAS_PER_SM;     // resident CTAs per SM the kernels are built for (<= 128 registers)
 constexpr int kMaxChannels = 148 * kCtasPerSm;     // hard cap on CTAs per rank per op
-constexpr int kDefaultChannels = 296;              // channels of a one-rank-per-GPU comm unless HETCCL_NCHANNELS
+constexpr int kDefaultChannels = kMaxChannels;     // channels of a one-rank-per-GPU comm unless HETCCL_NCHANNELS
+                                                   // (r02w, 2+2 / 1+1: 592 channels 592 / 572 GB/s, 296: 566 / 512)
 constexpr int kMaxSlots = 16;      // cap on the scratch ring depth per channel (HETCCL_NSLOTS)
 #ifndef HETCCL_THREADS
 #define HETCCL_THREADS 128
@@ -155,5 +156,6 @@ int nvls_create(int n, const int* devs, const Topo& t, size_t bytes_per_rank, in
 void nvls_destroy(NvlsState* s);
 void nvls_buffer(const NvlsState* s, void** p, size_t* bytes);
 int nvls_supports(const NvlsState* s, int dt, int red, const void* send, const void* recv);
+int nvls_aliases_staging(const NvlsState* s, int dt, const void* p, size_t bytes);
 
 }  // namespace hetccl

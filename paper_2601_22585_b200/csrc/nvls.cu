@@ -12,9 +12,14 @@
 //      narrows once, and multimem.st's the result into every member's uc (one store, the switch
 //      replicates), ACKs the cross slots (N_XACK) and signals N_OUT;
 //   4. after N_OUT from every member, copies uc -> y.
-// When send == recv == the uc buffer itself (hetccl_comm_nvls), steps 1 and 4 are skipped (zero copy).
+// 16-bit dtypes are staged in fp32 (HETCCL_NVLS_WIDE=1, default): step 1 widens x into an fp32 uc, the
+// switch adds fp32 (round-to-nearest-even on every add, q33/q34 probe; its native 16-bit adds are not RNE)
+// and the partial is narrowed once (reading R6) — the same error bound as the oracle's fold, so R7's
+// elementwise 1e-2 gate holds — at twice the multicast bytes; the final value goes back through uc in fp32
+// (exact) and is narrowed on the way out. When send == recv == the uc buffer itself (hetccl_comm_nvls; f32,
+// or 16-bit with HETCCL_NVLS_WIDE=0), steps 1 and 4 are skipped (zero copy).
 // The switch's summation order inside a domain is not reading R3's ascending rank order, so this mode
-// is tolerance-only (R7 gate; R21); the cross-domain fold keeps R3's order.
+// is tolerance-only (R7 gate; R21), not bit-exact; the cross-domain fold keeps R3's order.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -131,7 +136,7 @@ struct NvlsArgs {
   char* xs[kMaxRanks];        // cross slots of member i of domain q (q == k: mine)
   uint64_t* fl[kMaxRanks];    // flag area of every rank
   size_t xs_slot;     // bytes of one (slot, sender domain) cross buffer = ce / d elements
-  int me, d, D, i, k, nch, zero_copy;
+  int me, d, D, i, k, nch, zero_copy, wide;
   int dmem[kMaxRanks];        // ranks of my domain, by index
   int xrank[kMaxRanks];       // rank of member i of domain q
   unsigned long long* err;
@@ -174,11 +179,39 @@ __device__ void nv_signal(const NvlsArgs& a, int ch, int ctr, const int* who, in
   if (lane < n && lane != skip) nv_red(nv_flag(a, who[lane], ch, ctr, a.me));
 }
 
-template <int DT>
+// W: 16-bit dtype staged through an fp32 uc (a group of V elements = 16 bytes of x = UB = 32 bytes of uc)
+template <int DT, bool W>
 __global__ void __launch_bounds__(kNvThreads) k_nvls_allreduce(NvlsArgs a) {
   using VV = NvVec<DT>;
   constexpr int V = VV::V;
   constexpr int ES = 16 / V;
+  constexpr size_t UB = W ? 32 : 16;  // uc / mc bytes per group
+  static_assert(!W || DT != DT_F32, "fp32 staging is for 16-bit dtypes");
+  using F32 = NvVec<DT_F32>;
+  auto widen_st = [&](char* dst, const uint4& w, bool multi) {  // W: one 16-bit group -> two fp32 vectors
+    uint4 lo, hi;
+#pragma unroll
+    for (int e = 0; e < 4; e++) {
+      F32::set(lo, e, VV::get(w, e));
+      F32::set(hi, e, VV::get(w, e + 4));
+    }
+    if (multi) {
+      mc_st(dst, lo);
+      mc_st(dst + 16, hi);
+    } else {
+      nv_st(dst, lo);
+      nv_st(dst + 16, hi);
+    }
+  };
+  auto narrow2 = [&](const uint4& lo, const uint4& hi) {  // two fp32 vectors -> one 16-bit group (RNE)
+    uint4 w;
+#pragma unroll
+    for (int e = 0; e < 4; e++) {
+      VV::set(w, e, F32::get(lo, e));
+      VV::set(w, e + 4, F32::get(hi, e));
+    }
+    return w;
+  };
   const int ch = blockIdx.x;
   const int tid = threadIdx.x, nth = blockDim.x;
   __shared__ int s_abort;
@@ -221,7 +254,8 @@ __global__ void __launch_bounds__(kNvThreads) k_nvls_allreduce(NvlsArgs a) {
               else reinterpret_cast<uint16_t*>(&w)[e] = *(const uint16_t*)(a.send + (c0 + v * V + e) * 2);
             }
           }
-          nv_st(a.uc + v * 16, w);
+          if (W) widen_st(a.uc + v * UB, w, false);
+          else nv_st(a.uc + v * UB, w);
         }
       }
       // every storing thread orders its unicast stores before the peers' reads through the multicast
@@ -242,7 +276,9 @@ __global__ void __launch_bounds__(kNvThreads) k_nvls_allreduce(NvlsArgs a) {
     const size_t so = (size_t)(G & 1) * a.D;  // slot base (in units of xs_slot) of this chunk
     // ---- 2. domain partial through the switch -> my cross slot + member i of every other domain ----
     for (size_t v = lo + tid; v < hi; v += nth) {
-      const uint4 p = mc_ld_reduce<DT>(a.mc + v * 16);
+      uint4 p;
+      if (W) p = narrow2(mc_ld_reduce<DT_F32>(a.mc + v * UB), mc_ld_reduce<DT_F32>(a.mc + v * UB + 16));
+      else p = mc_ld_reduce<DT>(a.mc + v * UB);
       const size_t off = (v - (size_t)a.i * seg) * 16;
       for (int q = 0; q < a.D; q++) nv_st(a.xs[q] + (so + a.k) * a.xs_slot + off, p);
     }
@@ -272,7 +308,8 @@ __global__ void __launch_bounds__(kNvThreads) k_nvls_allreduce(NvlsArgs a) {
 #pragma unroll
         for (int e = 0; e < V; e++) VV::set(w, e, acc[e]);
       }
-      mc_st(a.mc + v * 16, w);
+      if (W) widen_st(a.mc + v * UB, w, true);
+      else mc_st(a.mc + v * UB, w);
     }
     __syncthreads();
     if (tid < 32) {
@@ -289,7 +326,7 @@ __global__ void __launch_bounds__(kNvThreads) k_nvls_allreduce(NvlsArgs a) {
         size_t l2, h2;
         range(s, l2, h2);
         for (size_t v = l2 + tid; v < h2; v += nth) {
-          const uint4 w = nv_ld(a.uc + v * 16);
+          const uint4 w = W ? narrow2(nv_ld(a.uc + v * UB), nv_ld(a.uc + v * UB + 16)) : nv_ld(a.uc + v * UB);
           if ((v + 1) * V <= len) {
             nv_st(a.recv + (c0 + v * V) * ES, w);
           } else {
@@ -370,6 +407,7 @@ struct McShared {  // one multicast object per domain, released with its last me
 
 struct NvlsState {
   int dev = 0, rank = 0, nch = 0;
+  int wide = 1;              // HETCCL_NVLS_WIDE: 16-bit dtypes staged in fp32 (R7-gate accuracy)
   size_t bytes = 0;          // uc / mc bytes
   size_t ce_bytes = 0;       // chunk bytes per rank (multiple of 16 * d)
   CUmemGenericAllocationHandle uc_h = 0;
@@ -478,6 +516,8 @@ int nvls_create(int n, const int* devs, const Topo& t, size_t bytes_per_rank, in
     out[r]->nch = nch;
     out[r]->bytes = bytes;
     out[r]->ce_bytes = ce_bytes;
+    const char* w = getenv("HETCCL_NVLS_WIDE");
+    out[r]->wide = !(w && *w == '0');
   }
   auto fail = [&](const char* what, int code) {
     nv_err(err, errlen, what, code);
@@ -557,6 +597,14 @@ int nvls_create(int n, const int* devs, const Topo& t, size_t bytes_per_rank, in
   return 0;
 }
 
+// 1 if [p, p+bytes) overlaps the uc buffer while 16-bit data would be staged wide through it (the copy-in
+// would overwrite its own input): the caller rejects that (hetcclInvalidArgument)
+int nvls_aliases_staging(const NvlsState* s, int dt, const void* p, size_t bytes) {
+  if (!s || !s->wide || dtype_size(dt) != 2 || !p) return 0;
+  const uintptr_t a0 = (uintptr_t)p, u0 = (uintptr_t)s->uc;
+  return a0 < u0 + s->bytes && u0 < a0 + bytes;
+}
+
 void nvls_buffer(const NvlsState* s, void** p, size_t* bytes) {
   if (p) *p = s ? (void*)s->uc : nullptr;
   if (bytes) *bytes = s ? s->ce_bytes : 0;
@@ -573,19 +621,27 @@ cudaError_t nvls_allreduce(NvlsState* s, const void* send, void* recv, size_t co
                            unsigned long long* err, long long timeout_ns, cudaStream_t st) {
   NvlsArgs a = s->tmpl;
   const int es = dtype_size(dt);
+  const bool wide = s->wide && es == 2;
   a.send = (const char*)send;
   a.recv = (char*)recv;
   a.count = count;
-  a.ce = s->ce_bytes / es;
+  a.ce = s->ce_bytes / (wide ? 4 : es);  // elements per chunk: uc holds fp32 when staging wide
   a.err = err;
   a.timeout_ns = timeout_ns;
-  a.zero_copy = send == recv && (const char*)send == (const char*)s->uc && count * es <= s->ce_bytes &&
+  a.wide = wide;
+  a.zero_copy = !wide && send == recv && (const char*)send == (const char*)s->uc && count * es <= s->ce_bytes &&
                 (count * es) % 16 == 0;
   dim3 grid(s->nch), block(kNvThreads);
   switch (dt) {
-    case DT_BF16: k_nvls_allreduce<DT_BF16><<<grid, block, 0, st>>>(a); break;
-    case DT_F16: k_nvls_allreduce<DT_F16><<<grid, block, 0, st>>>(a); break;
-    default: k_nvls_allreduce<DT_F32><<<grid, block, 0, st>>>(a); break;
+    case DT_BF16:
+      if (wide) k_nvls_allreduce<DT_BF16, true><<<grid, block, 0, st>>>(a);
+      else k_nvls_allreduce<DT_BF16, false><<<grid, block, 0, st>>>(a);
+      break;
+    case DT_F16:
+      if (wide) k_nvls_allreduce<DT_F16, true><<<grid, block, 0, st>>>(a);
+      else k_nvls_allreduce<DT_F16, false><<<grid, block, 0, st>>>(a);
+      break;
+    default: k_nvls_allreduce<DT_F32, false><<<grid, block, 0, st>>>(a); break;
   }
   return cudaGetLastError();
 }

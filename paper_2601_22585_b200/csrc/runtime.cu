@@ -246,6 +246,9 @@ hetcclResult_t run_op(hetcclComm_t c, int op, const void* const* sends, void* co
   if (op == OP_ALLREDUCE && c->nvls && nvls_supports(c->nvls, dt, red, sends[0], recvs[0])) {
     if ((((uintptr_t)sends[0] | (uintptr_t)recvs[0]) & 15) != 0)
       return fail(c, hetcclInvalidArgument, "NVLS mode needs 16-byte aligned send/recv buffers");
+    if (nvls_aliases_staging(c->nvls, dt, sends[0], count * es) || nvls_aliases_staging(c->nvls, dt, recvs[0], count * es))
+      return fail(c, hetcclInvalidArgument,
+                  "NVLS buffer is the fp32 staging area of 16-bit All-Reduces (HETCCL_NVLS_WIDE=1): use it for f32 only");
     CUDA_TRY(c, nvls_allreduce(c->nvls, sends[0], recvs[0], count, dt, c->err, c->timeout_ns, stream));
     return hetcclSuccess;
   }
@@ -333,10 +336,10 @@ hetcclResult_t run_op(hetcclComm_t c, int op, const void* const* sends, void* co
   // those): a deviation for NVSwitch (R20). HETCCL_FLAT_AG: 1 always, 0 never, unset = messages of
   // at most HETCCL_FLAT_AG_MAX_KB (32768) per rank, where one tile per channel walks the stages serially
   // and dropping one stage pays (q16, 2+2: 8 MiB +19%, 16 MiB +11%, 32 MiB +4%; 64 MiB and up ±0..2%).
-  // Rank-multiplexed comms take it at every size (stage D re-read y from HBM to forward it; r02k: 4+4 mux
-  // 430 -> 466 GB/s).
+  // With the TMA movers it pays at every size (r02k: 4+4 mux 430 -> 466 GB/s, stage D re-read y from HBM to
+  // forward it; r02w: 2+2 / 1+1 at 256 MiB 584 -> 592 / 544 -> 572 GB/s), so the band is unbounded by default.
   const long flat_env = env_long("HETCCL_FLAT_AG", -1);
-  const bool flat_band = c->kind == KIND_MUX || count * (size_t)es <= (size_t)env_long("HETCCL_FLAT_AG_MAX_KB", 32768) * 1024;
+  const bool flat_band = c->kind == KIND_MUX || count * (size_t)es <= (size_t)env_long("HETCCL_FLAT_AG_MAX_KB", 1L << 30) * 1024;
   if (a.direct && a.final_stage == 4 && c->topo.D > 1 && (flat_env == 1 || (flat_env < 0 && flat_band))) {
     a.flat_ag = 1;
     a.active &= ~(1u << 3);

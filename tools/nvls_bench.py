@@ -3,8 +3,9 @@
 python tools/nvls_bench.py [--gpus 4] [--maps 4,2+2] [--mibs 16,64,256] [--iters 20]
 Prints one JSON line per (map, size, mode): busBW = S * 2(n-1)/n / t, t = max over devices of the mean
 per-op time (CUDA events on each device's stream, all devices launched back to back every iteration).
-Modes: p2p (HETCCL_NVLS unset), nvls (copies in/out of the multicast-bound buffer), nvls_zc (in place
-on that buffer). Correctness: the R7 gate on rank 0's result against an fp64 sum of sampled windows.
+Modes: p2p (HETCCL_NVLS unset), nvls (copies in/out of the multicast-bound buffer, 16-bit staged in fp32),
+nvls_native16 (same with the switch's native 16-bit adds, HETCCL_NVLS_WIDE=0), nvls_zc (native, in place on
+that buffer). Correctness: the R7 gate on rank 0's result against an fp64 sum of sampled windows.
 """
 import argparse
 import json
@@ -33,12 +34,15 @@ def main():
         n = len(m)
         if n > torch.cuda.device_count():
             continue
-        for mode in ("p2p", "nvls", "nvls_zc"):
+        for mode in ("p2p", "nvls", "nvls_native16", "nvls_zc"):
             if mode == "p2p":
                 os.environ.pop("HETCCL_NVLS", None)
             else:
                 os.environ["HETCCL_NVLS"] = "1"
                 os.environ["HETCCL_NVLS_MB"] = str(max(mibs) if mode == "nvls_zc" else 32)
+                # nvls: 16-bit staged in fp32 (default, R7 gate); native16 / zc: the switch's own bf16 adds
+                # (HETCCL_NVLS_WIDE=0; not RNE, outside the parity bar - DESIGN.md R21)
+                os.environ["HETCCL_NVLS_WIDE"] = "1" if mode == "nvls" else "0"
             comms = hc.hetccl_comm_init_all(list(range(n)), m)
             on = hc.hetccl_comm_nvls(comms[0])[0]
             if mode != "p2p" and not on:

@@ -240,7 +240,7 @@ def main():
         for nstreams in (1, 2, 4):
             streams = [torch.cuda.Stream() for _ in range(nstreams)]
             # concurrent persistent kernels must be co-resident: split the SMs between the streams' comms
-            cs = [comm_for(name, m, slot=i, nch=296 // nstreams) for i in range(nstreams)]
+            cs = [comm_for(name, m, slot=i, nch=592 // nstreams) for i in range(nstreams)]  # 4 CTAs x 148 SMs
             outs = [hc.symmetric_empty(c, total, torch.bfloat16, group=gloo) for c in cs]
             out_g = outs[0]
             cur = torch.cuda.current_stream()
