@@ -415,12 +415,31 @@ def run_dist(args):
     okt = torch.tensor([1 if ok else 0], device="cuda")
     dist.all_reduce(okt, op=dist.ReduceOp.MIN)
 
-    # NCCL flat all-reduce on the same-size buffer (comparison baseline only)
+    # NCCL flat all-reduce on the same-size buffer (comparison baseline only): on a plain buffer (matched with
+    # our staged path) and on a buffer NCCL registered itself (torch.cuda.MemPool on NCCL's allocator +
+    # register_mem_pool: window registration, matched with our symmetric-buffer path)
     nbuf = send.clone()
     for _ in range(args.warmup):
         dist.all_reduce(nbuf)
     nccl_ms, _ = timed(lambda: dist.all_reduce(nbuf), args.steps)
     _, nccl_bus = busbw(S, nccl_ms / args.steps * 1e-3, world)
+    nccl_reg = {}
+    try:
+        backend = dist.group.WORLD._get_backend(torch.device("cuda", local))
+        pool = torch.cuda.MemPool(backend.mem_allocator)
+        with torch.cuda.use_mem_pool(pool):
+            rbuf = torch.empty_like(send)
+        backend.register_mem_pool(pool)
+        rbuf.copy_(send)
+        for _ in range(args.warmup):
+            dist.all_reduce(rbuf)
+        reg_ms, _ = timed(lambda: dist.all_reduce(rbuf), args.steps)
+        _, reg_bus = busbw(S, reg_ms / args.steps * 1e-3, world)
+        nccl_reg = {"busbw": round(reg_bus, 2)}
+        backend.deregister_mem_pool(pool)
+        del rbuf
+    except Exception as e:  # registration unavailable: say why, keep the plain comparison
+        nccl_reg = {"unavailable": f"{type(e).__name__}: {e}"[:200]}
 
     # e2e through the public API with pinned host buffers
     hin = torch.from_numpy(x.view(np.int16)).view(torch.bfloat16).pin_memory()
@@ -456,7 +475,14 @@ def run_dist(args):
                        "ranks": world, "rank_to_domain": m, "count": count, "l2": "inputs > L2 (no flush)",
                        "parallelism": f"dp{world}"},
             "algbw": round(alg, 2), "gpu_launches": args.steps * world,
-            "nccl_flat": {"busbw": round(nccl_bus, 2), "ratio": round(bus / nccl_bus, 4)},
+            "nccl_flat": {"busbw": round(nccl_bus, 2), "ratio": round(bus / nccl_bus, 4),
+                          "registered": nccl_reg,
+                          "matched": {"symmetric_vs_registered": round(bus / nccl_reg["busbw"], 4)
+                                      if "busbw" in nccl_reg else None,
+                                      "staged_vs_plain": round(staged_bus / nccl_bus, 4)},
+                          "note": "ratio = value (our symmetric buffers) / NCCL on a plain buffer; matched pairs: "
+                                  "ours on symmetric buffers vs NCCL on its own registered buffer, ours on plain "
+                                  "torch buffers vs NCCL on a plain buffer"},
             "staged_recv": {"busbw": round(staged_bus, 2),
                             "note": "send/recv in plain torch buffers: staged through scratch (value: symmetric buffers)"},
             "e2e": {"value": round(e2e_bus, 2), "unit": "GB/s", "h2d_bytes_per_step": world * S,

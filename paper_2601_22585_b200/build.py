@@ -11,11 +11,14 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libhetccl.so")
-SOURCES = ["kernels.cu", "runtime.cu", "plan.cpp", "nvls.cu"]
+# kernels.cu is compiled twice: as is (TMA movers, 4 CTAs per SM) and through kernels_legacy.cu (cp.async
+# movers, 2 CTAs per SM); the translation units compile in parallel, then link into one library
+SOURCES = ["kernels.cu", "kernels_legacy.cu", "runtime.cu", "plan.cpp", "nvls.cu"]
 HEADERS = ["hetccl_internal.h", os.path.join("..", "..", "include", "hetccl.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
-         "-Xcompiler", "-fPIC,-O2,-fvisibility=hidden", "-Xptxas", "-v", "--shared", "-cudart", "static"]
+CFLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
+          "-Xcompiler", "-fPIC,-O2,-fvisibility=hidden", "-Xptxas", "-v"]
+LDFLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "--shared", "-cudart", "static"]
 
 
 def stale():
@@ -32,15 +35,31 @@ def build(force=False, verbose=False, variant=None, defines=()):
     if not force and not variant and not stale():
         return LIB
     tmp = lib + f".tmp{os.getpid()}"
-    cmd = [NVCC, *FLAGS, *[f"-D{d}" for d in defines], "-o", tmp] + [os.path.join(CSRC, s) for s in SOURCES]
-    p = subprocess.run(cmd, capture_output=True, text=True)
+    objdir = os.path.join(HERE, "build", variant or "default")
+    os.makedirs(objdir, exist_ok=True)
+    procs = []
+    for src in SOURCES:
+        obj = os.path.join(objdir, os.path.splitext(src)[0] + ".o")
+        cmd = [NVCC, *CFLAGS, *[f"-D{d}" for d in defines], "-c", "-o", obj, os.path.join(CSRC, src)]
+        procs.append((src, obj, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
+    log = []
+    failed = False
+    for src, obj, p in procs:
+        out, err = p.communicate()
+        log.append(f"=== {src}\n{out}{err}")
+        if p.returncode != 0:
+            failed = True
+            sys.stderr.write(out + err)
+    if failed:
+        raise RuntimeError("nvcc failed building libhetccl.so")
+    p = subprocess.run([NVCC, *LDFLAGS, "-o", tmp] + [obj for _, obj, _ in procs], capture_output=True, text=True)
     if p.returncode != 0:
         sys.stderr.write(p.stdout + p.stderr)
-        raise RuntimeError("nvcc failed building libhetccl.so")
+        raise RuntimeError("nvcc failed linking libhetccl.so")
     with open(os.path.join(HERE, "ptxas_info.txt" if not variant else f"ptxas_info_{variant}.txt"), "w") as f:
-        f.write(p.stderr)
+        f.write("\n".join(log))
     if verbose:
-        sys.stderr.write(p.stderr)
+        sys.stderr.write("\n".join(log))
     os.replace(tmp, lib)
     return lib
 

@@ -19,18 +19,19 @@
 namespace hetccl {
 
 constexpr int kMaxRanks = 16;      // == HETCCL_MAX_RANKS (one flag line = 16 senders x 8 B)
-#ifndef HETCCL_CTAS_PER_SM
-#define HETCCL_CTAS_PER_SM 4
-#endif
-constexpr int kCtasPerSm = HETCCL_CTAS_PER_SM;     // resident CTAs per SM the kernels are built for (<= 128 registers)
-constexpr int kMaxChannels = 148 * kCtasPerSm;     // hard cap on CTAs per rank per op
-constexpr int kDefaultChannels = kMaxChannels;     // channels of a one-rank-per-GPU comm unless HETCCL_NCHANNELS
-                                                   // (r02w, 2+2 / 1+1: 592 channels 592 / 572 GB/s, 296: 566 / 512)
+// Two builds of the pipeline kernels (kernels.cu compiled twice):
+//   TMA kernels    (namespace k4): 4 CTAs per SM (<= 128 registers), sources staged by TMA bulk copies into a
+//                  shared-memory ring — the HBM-bound rank-multiplexed comms;
+//   legacy kernels (namespace k2): 2 CTAs per SM (<= 255 registers), sources staged by cp.async — the
+//                  NVLink-bound one-rank-per-GPU comms (the round-1 movers measured faster there, r02t/r02y).
+constexpr int kCtasPerSm = 4;                      // most resident CTAs per SM of any kernel build
+constexpr int kMaxChannels = 148 * kCtasPerSm;     // hard cap on CTAs per rank per op (flag area sizing)
+constexpr int kLegacyChannels = 148 * 2;           // default channels of a comm on the legacy kernels
 constexpr int kMaxSlots = 16;      // cap on the scratch ring depth per channel (HETCCL_NSLOTS)
 #ifndef HETCCL_THREADS
 #define HETCCL_THREADS 128
 #endif
-constexpr int kThreads = HETCCL_THREADS;  // threads per CTA (kCtasPerSm CTAs per SM)
+constexpr int kThreads = HETCCL_THREADS;  // threads per CTA
 constexpr int kMaxStages = 5;      // pipeline positions of the deepest op (All-Reduce)
 constexpr int kTraceWords = 10;    // per traced iteration: poll start, GO, DONE, fenced, end of stages 0..3;
                                    // iteration 0 also: kernel entry, kernel exit (after the final wait)

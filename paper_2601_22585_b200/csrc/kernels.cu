@@ -37,7 +37,20 @@
 
 #include "hetccl_internal.h"
 
+// This file is compiled twice (hetccl_internal.h): as is -> namespace hetccl::k4 (TMA movers, 4 CTAs per SM),
+// and through kernels_legacy.cu -> namespace hetccl::k2 (cp.async movers, 2 CTAs per SM, no TMA ring).
+#ifndef HETCCL_KNS
+#define HETCCL_KNS k4
+#endif
+#ifndef HETCCL_KERNEL_CPS
+#define HETCCL_KERNEL_CPS 4
+#endif
+#ifndef HETCCL_LEGACY_MOVERS
+#define HETCCL_LEGACY_MOVERS 0
+#endif
+
 namespace hetccl {
+namespace HETCCL_KNS {
 
 // ------------------------------------------------------------------ PTX primitives -------------
 // Flag operations at system scope (peers are other GPUs, over NVLink) or — when every rank of the
@@ -216,18 +229,18 @@ __device__ __forceinline__ void prefetch_ahead(const void* src, size_t v0, int t
 #ifndef HETCCL_TMA
 #define HETCCL_TMA 1
 #endif
-#ifndef HETCCL_STAGE_SMEM
-#define HETCCL_STAGE_SMEM (!HETCCL_TMA)  // the TMA ring replaces the cp.async staging (shared memory budget)
-#endif
+
 // Fold sources are staged through shared memory with cp.async (LDGSTS): each data thread issues the
 // 16-byte loads of up to kStageSrc sources x kUnroll vectors at once and waits once, so a fold keeps
 // kStageSrc times the bytes in flight that register loads (one source at a time) could, without the
 // registers. Each thread reads back only the slots it filled itself (no CTA barrier).
 constexpr int kStageSrc = 5;
 constexpr int kStageVecs = kStageSrc * kUnroll;  // 16-byte slots per data thread
-#if HETCCL_STAGE_SMEM
-__shared__ __align__(16) uint4 g_stage[kStageVecs * kThreads];
-#endif
+// the staging slots live in the dynamic shared memory of the legacy (2 CTAs per SM) kernels
+extern __shared__ __align__(128) unsigned char g_ring[];
+#define g_stage ((uint4*)g_ring)
+constexpr size_t kStageBytes = (size_t)kStageVecs * kThreads * 16;
+__shared__ int g_lgsts;  // 1: the movers stage through g_stage (legacy kernels), 0: TMA ring or register loads
 __device__ __forceinline__ void cp_async16(uint4* sdst, const void* gsrc) {
   const uint32_t sa = (uint32_t)__cvta_generic_to_shared(sdst);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gsrc) : "memory");
@@ -270,7 +283,6 @@ __shared__ unsigned g_seq;  // chunks this CTA has issued/consumed so far (all d
 __shared__ int g_tma;       // 1: the ring is initialised and the op may use it
 __shared__ const char* g_ops[kMaxList + kMaxRanks];  // operands of the current call, in load order
 __shared__ char* g_dst[kMaxList];                     // destinations of the current call
-extern __shared__ __align__(128) unsigned char g_ring[];
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
@@ -329,7 +341,8 @@ __device__ __forceinline__ void data_bar() { asm volatile("bar.sync 1, %0;" ::"r
 // all but the sync warp in the warp-specialised mode)
 __device__ __forceinline__ void tma_init(int enable, int data_warps, int l2hint) {
   if (threadIdx.x == 0) {
-    g_tma = HETCCL_TMA && enable;
+    g_tma = HETCCL_TMA && !HETCCL_LEGACY_MOVERS && enable;
+    g_lgsts = HETCCL_LEGACY_MOVERS;
     g_l2hint = l2hint;
     g_seq = 0;
     if (g_tma) {
@@ -550,7 +563,7 @@ __device__ __noinline__ void cta_fold(const PtrList& srcs, const PtrList& dsts, 
     tma_move<T, OP, 1>(srcs, -1, none, dsts, nv);
     nvr = 0;
   }
-#if HETCCL_STAGE_SMEM
+  if (g_lgsts) {  // round-1 movers: cp.async staging of the fold sources (legacy kernels)
   for (size_t v0 = tid; v0 < nvr; v0 += (size_t)kUnroll * nth) {
     for (int s = 0; s < srcs.n; s++) prefetch_ahead(srcs.p[s], v0, tid, (size_t)kUnroll * nth, nv);
     A acc[kUnroll][V];
@@ -577,7 +590,21 @@ __device__ __noinline__ void cta_fold(const PtrList& srcs, const PtrList& dsts, 
         }
       }
     }
-#else
+    uint4 o[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; u++)
+#pragma unroll
+      for (int e = 0; e < V; e++) Vec<S>::set(o[u], e, TR::narrow(acc[u][e]));
+    for (int d = 0; d < dsts.n; d++) {
+      char* dp = (char*)dsts.p[d];
+#pragma unroll
+      for (int u = 0; u < kUnroll; u++) {
+        size_t v = v0 + (size_t)u * nth;
+        if (v < nv) st_v4(dp + v * 16, o[u]);
+      }
+    }
+  }
+  } else {
   for (size_t v0 = tid; v0 < nvr; v0 += (size_t)kUnroll * nth) {
     for (int s = 0; s < srcs.n; s++) prefetch_ahead(srcs.p[s], v0, tid, (size_t)kUnroll * nth, nv);
     A acc[kUnroll][V];
@@ -607,7 +634,6 @@ __device__ __noinline__ void cta_fold(const PtrList& srcs, const PtrList& dsts, 
 #pragma unroll
         for (int e = 0; e < V; e++) acc[u][e] = comb<OP>(acc[u][e], TR::widen(Vec<S>::get(w[u], e)));
     }
-#endif
     uint4 o[kUnroll];
 #pragma unroll
     for (int u = 0; u < kUnroll; u++)
@@ -621,6 +647,7 @@ __device__ __noinline__ void cta_fold(const PtrList& srcs, const PtrList& dsts, 
         if (v < nv) st_v4(dp + v * 16, o[u]);
       }
     }
+  }
   }
   for (size_t i = nv * V + tid; i < n; i += nth) {
     A a;
@@ -663,7 +690,7 @@ __device__ __noinline__ void cta_fold_hier(const PtrList& inner, int kpos, const
     tma_move<T, OP, 2>(inner, kpos, outer, dsts, nv);
     nvr = 0;
   }
-#if HETCCL_STAGE_SMEM
+  if (g_lgsts) {  // round-1 movers: cp.async staging of the fold sources (legacy kernels)
   // operand list in load order: inner[0..inner.n), then outer[q] for q != kpos ascending; staged in groups
   // of kStageSrc (at 4+4 all five operands of a tile batch are in flight at once)
   const int L = inner.n + D - 1;
@@ -733,7 +760,21 @@ __device__ __noinline__ void cta_fold_hier(const PtrList& inner, int kpos, const
         }
       }
     }
-#else
+    uint4 o[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; u++)
+#pragma unroll
+      for (int e = 0; e < V; e++) Vec<S>::set(o[u], e, TR::narrow(acc[u][e]));
+    for (int d = 0; d < dsts.n; d++) {
+      char* dp = (char*)dsts.p[d];
+#pragma unroll
+      for (int u = 0; u < kUnroll; u++) {
+        size_t v = v0 + (size_t)u * nth;
+        if (v < nv) st_v4(dp + v * 16, o[u]);
+      }
+    }
+  }
+  } else {
   for (size_t v0 = tid; v0 < nvr; v0 += (size_t)kUnroll * nth) {
     for (int s = 0; s < inner.n; s++) prefetch_ahead(inner.p[s], v0, tid, (size_t)kUnroll * nth, nv);
     for (int q = 0; q < D; q++)
@@ -788,7 +829,6 @@ __device__ __noinline__ void cta_fold_hier(const PtrList& inner, int kpos, const
           acc[u][e] = q == 0 ? x : comb<OP>(acc[u][e], x);
         }
     }
-#endif
     uint4 o[kUnroll];
 #pragma unroll
     for (int u = 0; u < kUnroll; u++)
@@ -802,6 +842,7 @@ __device__ __noinline__ void cta_fold_hier(const PtrList& inner, int kpos, const
         if (v < nv) st_v4(dp + v * 16, o[u]);
       }
     }
+  }
   }
   for (size_t i = nv * V + tid; i < n; i += nth) {
     A a = 0;
@@ -1767,32 +1808,32 @@ struct A2aOp {
 
 // ================================================================== kernels ===================
 template <typename T, int OP>
-__global__ void __launch_bounds__(kThreads, kCtasPerSm) k_allreduce(const __grid_constant__ OpArgs a) {
+__global__ void __launch_bounds__(kThreads, HETCCL_KERNEL_CPS) k_allreduce(const __grid_constant__ OpArgs a) {
   ArOp<T, OP> op(a, blockIdx.y, blockIdx.x);
   run_pipeline(a, op, op.me, blockIdx.x);
 }
 template <typename T, int OP>
-__global__ void __launch_bounds__(kThreads, kCtasPerSm) k_reduce_scatter(const __grid_constant__ OpArgs a) {
+__global__ void __launch_bounds__(kThreads, HETCCL_KERNEL_CPS) k_reduce_scatter(const __grid_constant__ OpArgs a) {
   RsOp<T, OP> op(a, blockIdx.y, blockIdx.x);
   run_pipeline(a, op, op.me, blockIdx.x);
 }
 template <typename T>
-__global__ void __launch_bounds__(kThreads, kCtasPerSm) k_all_gather(const __grid_constant__ OpArgs a) {
+__global__ void __launch_bounds__(kThreads, HETCCL_KERNEL_CPS) k_all_gather(const __grid_constant__ OpArgs a) {
   AgOp<T> op(a, blockIdx.y, blockIdx.x);
   run_pipeline(a, op, op.me, blockIdx.x);
 }
 template <typename T, int OP>
-__global__ void __launch_bounds__(kThreads, kCtasPerSm) k_reduce(const __grid_constant__ OpArgs a) {
+__global__ void __launch_bounds__(kThreads, HETCCL_KERNEL_CPS) k_reduce(const __grid_constant__ OpArgs a) {
   RdOp<T, OP> op(a, blockIdx.y, blockIdx.x);
   run_pipeline(a, op, op.me, blockIdx.x);
 }
 template <typename T>
-__global__ void __launch_bounds__(kThreads, kCtasPerSm) k_all_to_all(const __grid_constant__ OpArgs a) {
+__global__ void __launch_bounds__(kThreads, HETCCL_KERNEL_CPS) k_all_to_all(const __grid_constant__ OpArgs a) {
   A2aOp<T> op(a, blockIdx.y, blockIdx.x);
   run_pipeline(a, op, op.me, blockIdx.x);
 }
 template <typename T>
-__global__ void __launch_bounds__(kThreads, kCtasPerSm) k_broadcast(const __grid_constant__ OpArgs a) {
+__global__ void __launch_bounds__(kThreads, HETCCL_KERNEL_CPS) k_broadcast(const __grid_constant__ OpArgs a) {
   BcOp<T> op(a, blockIdx.y, blockIdx.x);
   run_pipeline(a, op, op.me, blockIdx.x);
 }
@@ -1804,7 +1845,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_broadcast(const __grid
 // order (cta_fold_domains) — bitwise identical to the hierarchical path, one round trip.
 // Counters per (channel, sender): C_OS (data of op g landed), C_OSACK (op g's buffer consumed).
 template <typename T, int OP>
-__global__ void __launch_bounds__(kThreads, kCtasPerSm) k_allreduce_oneshot(const __grid_constant__ OpArgs a) {
+__global__ void __launch_bounds__(kThreads, HETCCL_KERNEL_CPS) k_allreduce_oneshot(const __grid_constant__ OpArgs a) {
   constexpr int V = Tr<T>::V;
   const int row = blockIdx.y, ch = blockIdx.x;
   const int me = a.local_rank[row], n = a.topo.n;
@@ -1821,6 +1862,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_allreduce_oneshot(cons
     g_dnth = blockDim.x;
     g_pf = 1;
     g_tma = 0;  // no ring in the one-shot kernel (its movers take the register path)
+    g_lgsts = 0;
   }
   __syncthreads();
   const unsigned long long g = ops0;
@@ -1956,7 +1998,11 @@ static KernFn pick(int op, int dt, int red) {
 }
 
 // dynamic shared memory of a launch: the TMA ring for the pipeline kernels when the op uses it
-static size_t dyn_smem(int op, int tma) { return (HETCCL_TMA && tma && op != OP_ALLREDUCE_ONESHOT) ? (size_t)kTmaStages * kTmaStageBytes : 0; }
+static size_t dyn_smem(int op, int tma) {
+  if (op == OP_ALLREDUCE_ONESHOT) return 0;
+  if (HETCCL_LEGACY_MOVERS) return kStageBytes;  // cp.async staging slots
+  return (HETCCL_TMA && tma) ? (size_t)kTmaStages * kTmaStageBytes : 0;
+}
 
 static cudaError_t allow_smem(KernFn fn, size_t bytes) {
   if (bytes == 0) return cudaSuccess;  // (static + dynamic > 48 KiB needs the opt-in even for 48 KiB dynamic)
@@ -1997,4 +2043,5 @@ int max_coresident(int op, int dt, int red, int tma) {
   return per_sm * sms;
 }
 
+}  // namespace HETCCL_KNS
 }  // namespace hetccl

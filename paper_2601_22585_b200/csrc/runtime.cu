@@ -17,9 +17,15 @@
 #include "hetccl_internal.h"
 
 namespace hetccl {
+namespace k4 {  // kernels.cu: TMA movers, 4 CTAs per SM
 cudaError_t launch_collective(const OpArgs& a, int nlocal, int dt, int red, bool cooperative, cudaStream_t s);
 cudaError_t launch_copy(const void* src, void* dst, size_t n, int es, cudaStream_t s);
 int max_coresident(int op, int dt, int red, int tma);
+}  // namespace k4
+namespace k2 {  // kernels_legacy.cu: cp.async movers, 2 CTAs per SM
+cudaError_t launch_collective(const OpArgs& a, int nlocal, int dt, int red, bool cooperative, cudaStream_t s);
+int max_coresident(int op, int dt, int red, int tma);
+}  // namespace k2
 cudaError_t nvls_allreduce(NvlsState* s, const void* send, void* recv, size_t count, int dt, unsigned long long* err,
                            long long timeout_ns, cudaStream_t st);
 }  // namespace hetccl
@@ -47,6 +53,7 @@ struct hetcclComm {
   int ws = 0;                             // HETCCL_WS: 0 plain pipeline, k in 2..4 warp-specialised (spacing k)
   int direct = 1;                         // HETCCL_DIRECT: write All-Reduce results straight into peers' recv
   int tma = 1;                            // HETCCL_TMA: movers stage sources through the TMA shared-memory ring
+  int legacy = 0;                         // HETCCL_LEGACY: pipeline ops on the legacy kernels (k2), else k4
   int nslots = 8;                         // HETCCL_NSLOTS: scratch ring depth
   size_t os_bytes = 0;                    // HETCCL_ONESHOT_KB: one-shot AR up to this many bytes per rank
   size_t os_chan = 0;                     // bytes per (buffer, sender, channel): each channel owns its region
@@ -123,7 +130,11 @@ size_t alloc_bytes_for(const hetcclComm* c) {
 }
 
 void read_env(hetcclComm* c) {
-  c->nch_max = (int)std::max(1L, std::min((long)kMaxChannels, env_long("HETCCL_NCHANNELS", kDefaultChannels)));
+  // one-rank-per-GPU comms default to the legacy kernels (NVLink-bound; r02y/r02z), rank-multiplexed comms to
+  // the TMA kernels (HBM-bound; r02k)
+  c->legacy = env_long("HETCCL_LEGACY", c->kind == KIND_MUX ? 0 : 1) != 0;
+  c->nch_max = (int)std::max(1L, std::min((long)kMaxChannels,
+                                          env_long("HETCCL_NCHANNELS", c->legacy ? kLegacyChannels : kMaxChannels)));
   // scratch slot: HETCCL_SLOT_KB, else sized from this map so every op's default tile fits
   const long slot_kb = env_long("HETCCL_SLOT_KB", 0);
   c->slot_bytes = slot_kb > 0 ? (size_t)std::max(64L, slot_kb) * 1024
@@ -240,7 +251,7 @@ hetcclResult_t run_op(hetcclComm_t c, int op, const void* const* sends, void* co
   }
   DevGuard g(c->device);
   if (c->n == 1) {  // a9: recv <- send
-    if (recvs[0]) CUDA_TRY(c, launch_copy(sends[0], recvs[0], recv_elems(op, count, 1), es, stream));
+    if (recvs[0]) CUDA_TRY(c, k4::launch_copy(sends[0], recvs[0], recv_elems(op, count, 1), es, stream));
     return hetcclSuccess;
   }
   if (op == OP_ALLREDUCE && c->nvls && nvls_supports(c->nvls, dt, red, sends[0], recvs[0])) {
@@ -271,7 +282,8 @@ hetcclResult_t run_op(hetcclComm_t c, int op, const void* const* sends, void* co
   }
   int nch_max = c->nch_max;
   if (c->kind == KIND_MUX) {
-    int cap = max_coresident(oneshot ? OP_ALLREDUCE_ONESHOT : op, dt, red, c->tma);
+    const int cap = (c->legacy && !oneshot) ? k2::max_coresident(op, dt, red, c->tma)
+                                            : k4::max_coresident(oneshot ? OP_ALLREDUCE_ONESHOT : op, dt, red, c->tma);
     if (cap < nlocal) return fail(c, hetcclInternalError, "device cannot co-schedule %d ranks", nlocal);
     nch_max = std::min(nch_max, cap / nlocal);
   }
@@ -290,7 +302,7 @@ hetcclResult_t run_op(hetcclComm_t c, int op, const void* const* sends, void* co
     a.os_chan = c->os_chan;
     a.err = c->err;
     a.timeout_ns = c->timeout_ns;
-    CUDA_TRY(c, launch_collective(a, nlocal, dt, red, c->kind == KIND_MUX, stream));
+    CUDA_TRY(c, k4::launch_collective(a, nlocal, dt, red, c->kind == KIND_MUX, stream));
     return hetcclSuccess;
   }
   const size_t slot_elems = c->slot_bytes / (size_t)es;
@@ -338,8 +350,13 @@ hetcclResult_t run_op(hetcclComm_t c, int op, const void* const* sends, void* co
   // and dropping one stage pays (q16, 2+2: 8 MiB +19%, 16 MiB +11%, 32 MiB +4%; 64 MiB and up ±0..2%).
   // With the TMA movers it pays at every size (r02k: 4+4 mux 430 -> 466 GB/s, stage D re-read y from HBM to
   // forward it; r02w: 2+2 / 1+1 at 256 MiB 584 -> 592 / 544 -> 572 GB/s), so the band is unbounded by default.
+  // With unequal domains it would load the smallest domain's members (their pieces go to every member of the
+  // larger domains: 1+3's singleton sends 2S instead of S), so across GPUs it is on for equal domains only.
   const long flat_env = env_long("HETCCL_FLAT_AG", -1);
-  const bool flat_band = c->kind == KIND_MUX || count * (size_t)es <= (size_t)env_long("HETCCL_FLAT_AG_MAX_KB", 1L << 30) * 1024;
+  bool equal = true;
+  for (int k = 1; k < c->topo.D; k++) equal = equal && c->topo.dom_size[k] == c->topo.dom_size[0];
+  const bool flat_band = c->kind == KIND_MUX ||
+                         (equal && count * (size_t)es <= (size_t)env_long("HETCCL_FLAT_AG_MAX_KB", 1L << 30) * 1024);
   if (a.direct && a.final_stage == 4 && c->topo.D > 1 && (flat_env == 1 || (flat_env < 0 && flat_band))) {
     a.flat_ag = 1;
     a.active &= ~(1u << 3);
@@ -408,7 +425,8 @@ hetcclResult_t run_op(hetcclComm_t c, int op, const void* const* sends, void* co
     c->trace_shape[0] = nlocal;
     c->trace_shape[1] = geo.nch;
   }
-  CUDA_TRY(c, launch_collective(a, nlocal, dt, red, c->kind == KIND_MUX, stream));
+  if (c->legacy) CUDA_TRY(c, k2::launch_collective(a, nlocal, dt, red, c->kind == KIND_MUX, stream));
+  else CUDA_TRY(c, k4::launch_collective(a, nlocal, dt, red, c->kind == KIND_MUX, stream));
   return hetcclSuccess;
 }
 
@@ -596,8 +614,10 @@ hetcclResult_t hetccl_comm_init_mux(hetcclComm_t* comm, int nranks, const int* r
      // unless HETCCL_NCHANNELS caps it)
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, cuda_device);
+    c->legacy = env_long("HETCCL_LEGACY", 0) != 0;
+    const int cps = c->legacy ? 2 : kCtasPerSm;
     c->nch_max = (int)std::max(1L, std::min((long)kMaxChannels, env_long("HETCCL_NCHANNELS", kMaxChannels)));
-    c->nch_max = std::max(1, std::min(c->nch_max, sms * kCtasPerSm / nranks));
+    c->nch_max = std::max(1, std::min(c->nch_max, sms * cps / nranks));
     // few channels per rank: 1 MiB tiles amortise the per-iteration protocol (measured 262 -> 356 GB/s)
     c->tile_base = (size_t)1 << 20;
     const int nch = c->nch_max;

@@ -35,6 +35,8 @@ def main():
     ap.add_argument("--out", default=None)
     ap.add_argument("--iters", type=int, default=10)
     ap.add_argument("--mibs", default="1,2,4,8,16,32,64,128,256,512,1024", help="ar_sweep sizes (MiB per rank)")
+    ap.add_argument("--kibs", default=None, help="ar_sweep sizes in KiB per rank (overrides --mibs; 1 KiB - 1 MiB "
+                                                 "is the latency regime, NEXT-3)")
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -121,9 +123,10 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MIN)
         return bool(t.item())
 
-    def ar_row(name, m, mib, seed=2, iters=None):
-        count = mib * (1 << 20) // 2
+    def ar_row(name, m, mib, seed=2, iters=None, kib=None):
+        count = (kib * 1024 if kib is not None else mib * (1 << 20)) // 2
         S = count * 2
+        mib = S / (1 << 20)
         x = bf16_inputs(seed, count)
         y = torch.empty_like(x)
         c = comm_for(name, m)
@@ -154,14 +157,19 @@ def main():
               "vs_nccl": round(bus / nbus, 4), "busbw_over_900": round(bus / 900, 4),
               "link_util_770": round(busiest / t / 1e9 / 770, 4), "r7_gate": ok, "cuda_graph": graph,
               "staged_busbw": round(S / t_staged / 1e9 * 2 * (world - 1) / world, 2),
+              "us": round(t * 1e6, 2), "nccl_us": round(tn * 1e6, 2), "staged_us": round(t_staged * 1e6, 2),
               "note": "busbw: send/recv in symmetric buffers (pull + direct); staged_busbw: plain torch buffers"})
         del x, y, z
 
     if args.what == "ar_sweep":
         name = DEFAULT[world]
         m = SPLITS[world][name]
-        for mib in [int(v) for v in args.mibs.split(",")]:
-            ar_row(name, m, mib)
+        if args.kibs:
+            for kib in [int(v) for v in args.kibs.split(",")]:
+                ar_row(name, m, None, kib=kib)
+        else:
+            for mib in [int(v) for v in args.mibs.split(",")]:
+                ar_row(name, m, mib)
     elif args.what == "splits":
         for name, m in SPLITS[world].items():
             ar_row(name, m, 256)
