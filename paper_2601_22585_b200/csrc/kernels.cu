@@ -265,11 +265,11 @@ __device__ __forceinline__ void cp_async_wait_all() {
 //   g % kTmaStages; it is that stage's u-th use (u = g / kTmaStages): FULL phase parity u & 1, and before
 //   issuing it the producer waits for EMPTY completion u-1 (parity (u-1) & 1).
 #ifndef HETCCL_TMA_STAGES
-#define HETCCL_TMA_STAGES 3
+#define HETCCL_TMA_STAGES 2
 #endif
 #ifndef HETCCL_TMA_STAGE_KB
-#define HETCCL_TMA_STAGE_KB 16  // 3 x 16 KiB per CTA, 4 CTAs per SM (r02k: 2 CTAs x 4 x 24 KiB -10%)
-#endif
+#define HETCCL_TMA_STAGE_KB 24  // 2 x 24 KiB per CTA, 4 CTAs per SM: fewer, larger chunks beat deeper rings
+#endif                          // (r02ab/r02ac mux: 2x24 478-480, 2x26 475, 3x18 472, 3x16 456, 3x36 @3 CTAs 459)
 constexpr int kTmaStages = HETCCL_TMA_STAGES;
 constexpr int kTmaStageBytes = HETCCL_TMA_STAGE_KB * 1024;
 constexpr int kTmaMaxVpt = 4;  // 16-byte vectors per thread per operand per chunk (register bound of the fold)
