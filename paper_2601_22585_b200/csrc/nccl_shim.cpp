@@ -97,7 +97,7 @@ void attach(ncclComm_t comm, int nranks, int rank) {
   if (off && *off && *off != '0') return;
   std::vector<int> m;
   // same decision on every rank: nranks and the environment are shared
-  if (nranks < 2 || nranks > HETCCL_MAX_RANKS || !domain_map(nranks, &m)) return;
+  if (nranks < 1 || nranks > HETCCL_MAX_RANKS || !domain_map(nranks, &m)) return;  // (1 rank: the n = 1 copy path)
   int dev = 0;
   cudaGetDevice(&dev);
   const size_t all_bytes = (size_t)nranks * HETCCL_BLOB_BYTES;

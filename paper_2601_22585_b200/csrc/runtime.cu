@@ -281,6 +281,11 @@ hetcclResult_t run_op(hetcclComm_t c, int op, const void* const* sends, void* co
     a.local_rank[i] = c->kind == KIND_MUX ? i : c->rank;
   }
   int nch_max = c->nch_max;
+  if (c->kind != KIND_MUX) {  // every channel's CTA must be co-resident (the pipeline waits across channels)
+    const int cap = (c->legacy && !oneshot) ? k2::max_coresident(op, dt, red, c->tma)
+                                            : k4::max_coresident(oneshot ? OP_ALLREDUCE_ONESHOT : op, dt, red, c->tma);
+    if (cap > 0) nch_max = std::min(nch_max, cap);
+  }
   if (c->kind == KIND_MUX) {
     const int cap = (c->legacy && !oneshot) ? k2::max_coresident(op, dt, red, c->tma)
                                             : k4::max_coresident(oneshot ? OP_ALLREDUCE_ONESHOT : op, dt, red, c->tma);

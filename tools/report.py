@@ -8,6 +8,9 @@
 * c4          : 1.3e9-element gradients in 25 MiB buckets, issued round-robin on 1/2/4 streams (one comm per
                 stream), wall time per step vs NCCL
 * c5          : Llama-7B gradients (6,738,415,616 elements, 13.5 GB bf16 per rank) in 256 MiB buckets
+* channels    : AR 256 MiB at the default split with 16 / 32 / 64 / 148 / 296 CTAs per GPU (SM budget) vs NCCL
+* overlap     : 24 x 25 MiB buckets all-reduced on a comm stream beside a bf16 GEMM stream: overlap ratio
+                (t_gemm + t_comm - t_both) / min, NCCL and hetccl at 64 / 296 CTAs
 Times: CUDA events on the launching stream, max over ranks (R16). busBW per R15. Parity: each
 measured AR/RS buffer passes DESIGN.md R7's gate vs an fp64 sum on sampled windows (tests/ owns bitwise
 parity against the oracle); AG/Broadcast results are compared bitwise with NCCL's.
@@ -234,6 +237,85 @@ def main():
                   "busbw": round(S / t / 1e9 * f, 2), "nccl_busbw": round(S / tn / 1e9 * f, 2),
                   "vs_nccl": round(tn / t, 4), "equals_nccl_bitwise": ok})
             del x, y, ya, yb, yn, zb, yr, zr, y2, z2
+    elif args.what == "channels":
+        # SM budget: AR 256 MiB at the default split on symmetric buffers with 16..296 CTAs per GPU
+        name = DEFAULT[world]
+        m = SPLITS[world][name]
+        count = 128 << 20
+        x = bf16_inputs(2, count)
+        z = x.clone()
+        tn = timed(lambda: dist.all_reduce(z), args.iters)
+        nbus = count * 2 / tn / 1e9 * 2 * (world - 1) / world
+        for nch in (16, 32, 64, 148, 296):
+            c = comm_for(name, m, slot=100 + nch, nch=nch)
+            xs = hc.symmetric_empty(c, count, torch.bfloat16, group=gloo)
+            ys = hc.symmetric_empty(c, count, torch.bfloat16, group=gloo)
+            xs.copy_(x)
+            t = timed(lambda: hc.allreduce(xs, ys, c), args.iters)
+            ok = parity_ar(ys, 2, count, m)
+            bus = count * 2 / t / 1e9 * 2 * (world - 1) / world
+            emit({"row": "channels", "split": name, "n": world, "ctas_per_gpu": nch, "bytes": count * 2,
+                  "ms": round(t * 1e3, 4), "busbw": round(bus, 2), "nccl_busbw": round(nbus, 2),
+                  "vs_nccl": round(bus / nbus, 4), "r7_gate": ok})
+            hc.lib().hetccl_mem_free(c, ys.data_ptr())
+            hc.lib().hetccl_mem_free(c, xs.data_ptr())
+    elif args.what == "overlap":
+        # C4-style gradient buckets all-reduced on a comm stream while a bf16 GEMM stream runs:
+        # overlap = (t_gemm + t_comm - t_both) / min(t_gemm, t_comm), 1 = fully hidden, 0 = serialised
+        name = {2: "1+1", 4: "1+1+2", 8: "2+2+4"}[world]
+        m = SPLITS[world][name]
+        nb, bucket = 24, 25 * (1 << 20) // 2
+        g = bf16_inputs(4, nb * bucket)
+        A = torch.randn(8192, 8192, device="cuda").bfloat16()
+        B = torch.randn(8192, 8192, device="cuda").bfloat16()
+        C = torch.empty(8192, 8192, device="cuda", dtype=torch.bfloat16)
+        sg, sc = torch.cuda.Stream(), torch.cuda.Stream()
+        cur = torch.cuda.current_stream()
+
+        def gemm():
+            sg.wait_stream(cur)
+            with torch.cuda.stream(sg):
+                for _ in range(8):
+                    torch.matmul(A, B, out=C)
+            cur.wait_stream(sg)
+
+        def run(comm_fn, with_gemm):
+            def step():
+                sc.wait_stream(cur)
+                if with_gemm:
+                    sg.wait_stream(cur)
+                    with torch.cuda.stream(sg):
+                        for _ in range(8):
+                            torch.matmul(A, B, out=C)
+                with torch.cuda.stream(sc):
+                    comm_fn()
+                cur.wait_stream(sc)
+                if with_gemm:
+                    cur.wait_stream(sg)
+            return timed(step, 3, warm=1)
+        t_gemm = timed(gemm, 3, warm=1)
+        red = g.clone()
+
+        def nccl_fn():
+            for b in range(nb):
+                dist.all_reduce(red[b * bucket:(b + 1) * bucket])
+        rows = [("nccl", nccl_fn)]
+        for nch in (64, 296):
+            c = comm_for(name, m, slot=200 + nch, nch=nch)
+
+            def hc_fn(c=c):
+                for b in range(nb):
+                    hc.hetccl_allreduce(g[b * bucket:].data_ptr(), red[b * bucket:].data_ptr(), bucket, hc.BFLOAT16,
+                                        "sum", c, sc.cuda_stream)
+            rows.append((f"hetccl_{nch}ch", hc_fn))
+        for label, fn in rows:
+            t_comm = run(fn, False)
+            t_both = run(fn, True)
+            emit({"row": "overlap", "split": name, "n": world, "impl": label, "buckets": nb,
+                  "bytes": nb * bucket * 2, "gemm_ms": round(t_gemm * 1e3, 3), "comm_ms": round(t_comm * 1e3, 3),
+                  "both_ms": round(t_both * 1e3, 3),
+                  "overlap": round((t_gemm + t_comm - t_both) / min(t_gemm, t_comm), 4),
+                  "comm_busbw": round(nb * bucket * 2 / t_comm / 1e9 * 2 * (world - 1) / world, 2)})
     elif args.what == "c4":
         name = {2: "1+1", 4: "1+1+2", 8: "2+2+4"}[world]
         m = SPLITS[world][name]
@@ -248,7 +330,8 @@ def main():
         for nstreams in (1, 2, 4):
             streams = [torch.cuda.Stream() for _ in range(nstreams)]
             # concurrent persistent kernels must be co-resident: split the SMs between the streams' comms
-            cs = [comm_for(name, m, slot=i, nch=592 // nstreams) for i in range(nstreams)]  # 4 CTAs x 148 SMs
+            slots = 592 if os.environ.get("HETCCL_LEGACY") == "0" else 296  # CTAs per GPU of the kernel build
+            cs = [comm_for(name, m, slot=i, nch=slots // nstreams) for i in range(nstreams)]
             outs = [hc.symmetric_empty(c, total, torch.bfloat16, group=gloo) for c in cs]
             out_g = outs[0]
             cur = torch.cuda.current_stream()
