@@ -147,7 +147,9 @@ void read_env(hetcclComm* c) {
   c->tma = env_long("HETCCL_TMA", 1) != 0;
   if (c->ws == 1 || c->ws < 0) c->ws = 0;
   if (c->ws > 4) c->ws = 4;
-  c->nslots = (int)std::max(2L, std::min((long)kMaxSlots, env_long("HETCCL_NSLOTS", 8)));
+  // rank-multiplexed comms: 6 slots (the deepest op pipeline, staged All-Reduce, has 5 positions) of the larger
+  // tile; one-rank-per-GPU comms keep 8
+  c->nslots = (int)std::max(2L, std::min((long)kMaxSlots, env_long("HETCCL_NSLOTS", c->kind == KIND_MUX ? 6 : 8)));
   // one-shot cutoff: a rank pushes (n-1) x its buffer, so bound that (16 MiB) rather than the buffer
   // (measured with CUDA graphs: 1+1 one-shot beats the pipeline up to 16 MiB; 2+2 up to ~4 MiB)
   const long os_default_kb = c->topo.n > 1 ? 16384L / (c->topo.n - 1) : 0;
@@ -623,11 +625,21 @@ hetcclResult_t hetccl_comm_init_mux(hetcclComm_t* comm, int nranks, const int* r
     const int cps = c->legacy ? 2 : kCtasPerSm;
     c->nch_max = (int)std::max(1L, std::min((long)kMaxChannels, env_long("HETCCL_NCHANNELS", kMaxChannels)));
     c->nch_max = std::max(1, std::min(c->nch_max, sms * cps / nranks));
-    // few channels per rank: 1 MiB tiles amortise the per-iteration protocol (measured 262 -> 356 GB/s)
-    c->tile_base = (size_t)1 << 20;
+    // rank-multiplexed comms are HBM-bound and their CTAs share one device: large tiles (4 MiB per rank: one
+    // tile per channel up to ~300 MiB messages, so the kernel runs as two bulk phases with the least skew
+    // coupling; r02ai: 478 -> 497 GB/s at 4+4 256 MiB), shrunk while the scratch (ranks x channels x slots x
+    // slot) would exceed HETCCL_SCRATCH_GB (32)
+    c->tile_base = (size_t)4 << 20;
     const int nch = c->nch_max;
-    read_env(c);  // re-derive the slot from the larger tile
-    c->nch_max = nch;
+    const size_t budget = (size_t)std::max(1L, env_long("HETCCL_SCRATCH_GB", 32)) << 30;
+    for (;;) {
+      read_env(c);  // re-derive the slot from the tile
+      c->nch_max = nch;
+      if (c->tile_base <= ((size_t)256 << 10) ||
+          (size_t)nranks * (size_t)nch * (size_t)c->nslots * c->slot_bytes <= budget)
+        break;
+      c->tile_base /= 2;
+    }
     set_os_layout(c);
     c->alloc_bytes = alloc_bytes_for(c);
   }

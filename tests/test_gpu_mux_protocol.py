@@ -33,7 +33,7 @@ PROTOS = {
     # warp-specialised: consumers sit 2 positions after producers, so the ring must exceed 2*(stages-1)+2
     "sys_push_staged_ws2": {"HETCCL_SYS_SCOPE": "1", "HETCCL_PULL": "0", "HETCCL_DIRECT": "0", "HETCCL_WS": "2",
                             "HETCCL_NSLOTS": "12"},
-    "gpu_pull_ws2": {"HETCCL_SYS_SCOPE": "0", "HETCCL_WS": "2"},
+    "gpu_pull_ws2": {"HETCCL_SYS_SCOPE": "0", "HETCCL_WS": "2", "HETCCL_NSLOTS": "12"},
 }
 SPLITS = ["1+1", "2+2", "4+4", "2+6", "2+2+4", "1+2+3"]
 
