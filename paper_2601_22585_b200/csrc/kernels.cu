@@ -464,6 +464,153 @@ __device__ __noinline__ void tma_stream(int ni, int D, int kpos, int nd, uint32_
   *(volatile unsigned*)&g_seq = seq0 + nchunks;  // every data thread writes the same value
 }
 
+// ---- chunk stealing inside the ring (HETCCL_STEAL; the C stage of All-Reduce) ----------------------------
+// A job is one mover call's chunks, published in a 64-bit word W = tag(16) << 48 | total(24) << 24 | count(24)
+// (tag = tile index << 4 | slot of the owning channel; flags line kCounters, word 0, of (rank, channel); word 1
+// counts the chunks other channels completed). The owner and any helper claim kClaimBatch chunks at a time with
+// one atomicAdd on W, issued a batch AHEAD by the producer thread so the claim's latency hides behind the
+// chunks in flight; the claimed index rides to the consumers in g_chunk_of[stage], and an exhausted claim sends
+// a sentinel stage (plain arrive, no bytes) that ends the call. An add that lands on an exhausted word is
+// harmless (count only grows past total); jobs are only published when every channel has one tile, so a word
+// never changes job while a helper holds its tag.
+constexpr uint32_t kClaimBatch = 4;
+__shared__ uint64_t* g_claim;    // job word of the current dynamic call, or null
+__shared__ int g_claim_mode;     // 0 static chunks, 1 owner (publishes W), 2 helper
+__shared__ uint64_t g_claim_tag; // the tag the call's operand lists were built for
+__shared__ unsigned g_claimed;   // chunks this CTA processed in its last dynamic call
+__shared__ unsigned g_job_total; // chunks of the job the owner published (0: none)
+__shared__ int g_vec_only;       // 1: the fold movers run only their TMA vector part (helpers; no scalar tail)
+__shared__ int g_chunk_of[kTmaStages];
+__device__ __forceinline__ void st_release_gpu(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire_gpu(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t fetch_add_acq_rel(uint64_t* p, uint64_t v) {
+  uint64_t old;
+  asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
+  return old;
+}
+constexpr uint64_t kTagMask = ~((1ull << 48) - 1);
+
+template <typename T, int OP, int MODE>
+__device__ __noinline__ void tma_stream_dyn(int ni, int D, int kpos, int nd, uint32_t nv, unsigned seq0) {
+  using TR = Tr<T>;
+  using S = typename TR::S;
+  using A = typename TR::A;
+  constexpr int V = TR::V;
+  const int tid = (int)threadIdx.x - g_dbase, nth = g_dnth;
+  const int nops = MODE == 2 ? ni + D - 1 : (MODE == 1 ? ni : 1);
+  const uint32_t cv = min((uint32_t)(kTmaStageBytes / (nops * 16)) / kTmaAlignV * kTmaAlignV, (uint32_t)(kTmaMaxVpt * nth));
+  const uint32_t chb = cv * 16;
+  const uint32_t nchunks = (nv + cv - 1) / cv;
+  const int mode = g_claim_mode;
+  uint64_t* w = g_claim;
+  const uint64_t tag = g_claim_tag;
+  const int hint = g_l2hint & 1;
+  const uint64_t pol_first = policy_evict_first();
+  if (mode == 1 && tid == 0) {
+    *(volatile uint64_t*)(w + 1) = 0;
+    g_job_total = nchunks;
+    st_release_gpu(w, tag | ((uint64_t)nchunks << 24));  // count 0
+  }
+  // (producer) claims: the batch being used and the one claimed ahead of it
+  bool ended = false;                  // the sentinel is issued
+  uint64_t ahead = 0;                  // W before the add that claimed the next batch
+  uint32_t cur = 0, cur_end = 0;       // chunks [cur, cur_end) of the current batch are left
+  auto claim_batch = [&]() -> uint64_t { return fetch_add_acq_rel(w, kClaimBatch); };
+  auto next_chunk = [&]() -> long long {
+    if (cur >= cur_end) {  // take the batch claimed ahead, claim the next one
+      const uint64_t tot = (ahead >> 24) & 0xffffffull, cnt = ahead & 0xffffffull;
+      if ((ahead & kTagMask) != tag || cnt >= tot) return -1;
+      cur = (uint32_t)cnt;
+      cur_end = (uint32_t)min(tot, cnt + kClaimBatch);
+      ahead = claim_batch();
+    }
+    return cur++;
+  };
+  auto issue = [&](uint32_t k) {
+    const unsigned g = seq0 + k, st = g % kTmaStages, u = g / kTmaStages;
+    if (u > 0) mbar_wait(&g_empty[st], (u - 1) & 1u);
+    const long long c = next_chunk();
+    *(volatile int*)&g_chunk_of[st] = (int)c;
+    if (c < 0) {
+      ended = true;
+      mbar_arrive(&g_full[st]);  // sentinel: completes the phase with no bytes
+      return;
+    }
+    const uint32_t bytes = min(cv, nv - (uint32_t)c * cv) * 16;
+    mbar_arrive_expect_tx(&g_full[st], bytes * (uint32_t)nops);
+    for (int j = 0; j < nops; j++) {
+      if (hint) bulk_g2s_hint(g_ring + st * kTmaStageBytes + j * chb, g_ops[j] + (size_t)c * chb, bytes, &g_full[st], pol_first);
+      else bulk_g2s(g_ring + st * kTmaStageBytes + j * chb, g_ops[j] + (size_t)c * chb, bytes, &g_full[st]);
+    }
+  };
+  if (tid == 0) ahead = claim_batch();
+  if (tid == 0)
+    for (uint32_t k = 0; k < (uint32_t)kTmaStages - 1 && !ended; k++) issue(k);
+  const int lane = threadIdx.x & 31;
+  uint32_t k = 0, mine = 0;
+  for (;;) {
+    if (tid == 0 && !ended) issue(k + kTmaStages - 1);
+    const unsigned g = seq0 + k, st = g % kTmaStages;
+    mbar_wait(&g_full[st], (g / kTmaStages) & 1u);
+    const int c = *(volatile int*)&g_chunk_of[st];
+    k++;
+    if (c < 0) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&g_empty[st]);
+      break;
+    }
+    const unsigned char* sb = g_ring + st * kTmaStageBytes;
+    const uint32_t lim = min(cv, nv - (uint32_t)c * cv);
+    for (uint32_t idx = tid; idx < lim; idx += nth) {
+      uint4 o = *(const uint4*)(sb + idx * 16);
+      if (MODE != 0) {
+        A acc[V];
+#pragma unroll
+        for (int e = 0; e < V; e++) acc[e] = TR::widen(Vec<S>::get(o, e));
+#pragma unroll 1
+        for (int j = 1; j < ni; j++) {
+          const uint4 wv = *(const uint4*)(sb + j * chb + idx * 16);
+#pragma unroll
+          for (int e = 0; e < V; e++) acc[e] = comb<OP>(acc[e], TR::widen(Vec<S>::get(wv, e)));
+        }
+        if (MODE == 2) {
+          uint4 pk;
+#pragma unroll
+          for (int e = 0; e < V; e++) Vec<S>::set(pk, e, TR::narrow(acc[e]));
+          const uint4 w0 = kpos == 0 ? pk : *(const uint4*)(sb + ni * chb + idx * 16);
+#pragma unroll
+          for (int e = 0; e < V; e++) acc[e] = TR::widen(Vec<S>::get(w0, e));
+#pragma unroll 1
+          for (int q = 1; q < D; q++) {
+            const uint4 wv = q == kpos ? pk : *(const uint4*)(sb + (ni + (q < kpos ? q : q - 1)) * chb + idx * 16);
+#pragma unroll
+            for (int e = 0; e < V; e++) acc[e] = comb<OP>(acc[e], TR::widen(Vec<S>::get(wv, e)));
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < V; e++) Vec<S>::set(o, e, TR::narrow(acc[e]));
+      }
+      const size_t off = ((size_t)c * cv + idx) * 16;
+      if (hint) {
+        for (int d = 0; d < nd; d++) st_v4_hint(g_dst[d] + off, o, pol_first);
+      } else {
+        for (int d = 0; d < nd; d++) st_v4(g_dst[d] + off, o);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&g_empty[st]);
+    mine++;
+  }
+  *(volatile unsigned*)&g_seq = seq0 + k;  // every data thread writes the same values
+  *(volatile unsigned*)&g_claimed = mine;
+}
+
 // Vector part (nv 16-byte vectors) of the three movers through the ring:
 //   MODE 0 copy : dst[d] = inner[0] (bits)
 //   MODE 1 fold : dst[d] = narrow(fold_{s} widen(inner[s]))
@@ -489,7 +636,8 @@ __device__ __forceinline__ void tma_move(const PtrList& inner, int kpos, const P
     g_dead_ops = dm;
   }
   data_bar();
-  tma_stream<T, OP, MODE>(ni, D, kpos, nd, (uint32_t)nv, seq0);
+  if (MODE == 2 && g_claim_mode) tma_stream_dyn<T, OP, MODE>(ni, D, kpos, nd, (uint32_t)nv, seq0);
+  else tma_stream<T, OP, MODE>(ni, D, kpos, nd, (uint32_t)nv, seq0);
 }
 
 // dst[d][i] = src[i] for every destination d, i < n elements of size ES (bit copy)
@@ -690,6 +838,7 @@ __device__ __noinline__ void cta_fold_hier(const PtrList& inner, int kpos, const
     tma_move<T, OP, 2>(inner, kpos, outer, dsts, nv);
     nvr = 0;
   }
+  if (g_vec_only) return;  // a stealing helper: the owner does everything the ring does not
   if (g_lgsts) {  // round-1 movers: cp.async staging of the fold sources (legacy kernels)
   // operand list in load order: inner[0..inner.n), then outer[q] for q != kpos ascending; staged in groups
   // of kStageSrc (at 4+4 all five operands of a tile batch are in flight at once)
@@ -1075,10 +1224,91 @@ struct Pipe {
     if (last >= 0 && tile_at(it, last, tl)) red_add_relaxed(chan_flags(a, lane, ch) + C_ACK * kLineWords + me, 1, a.gpu_scope);
   }
   unsigned long long* trc = nullptr;  // per-iteration stamps (HETCCL_TRACE_ITERS), thread 0 only
+  // C stage of my tile t with chunk stealing (owner side); false if the job cannot be shared (several pieces)
+  __device__ bool owner_c(size_t t, int slot, long long tl) {
+    if constexpr (!Op::kSteal) {
+      return false;
+    } else {
+      if (ntl != 1 || tl >= 4096 || slot >= 16 || op.c_pieces(t) != 1) return false;
+      const int tid = (int)threadIdx.x - g_dbase;
+      uint64_t* sw = chan_flags(a, me, ch) + (size_t)kCounters * kLineWords;
+      if (tid == 0) {
+        g_claim = sw;
+        g_claim_mode = 1;
+        g_claim_tag = ((uint64_t)tl << 52) | ((uint64_t)slot << 48);
+        g_job_total = 0;
+        g_claimed = 0;
+      }
+      data_bar();
+      op.stage(2, t, slot);  // its ring mover publishes the job and claims from the front
+      data_bar();
+      if (tid == 0) {
+        g_claim_mode = 0;
+        const uint64_t total = g_job_total, mine = g_claimed;
+        const uint64_t t0 = globaltimer();
+        uint32_t spins = 0;
+        while (total > mine && ld_acquire_gpu(sw + 1) < total - mine) {  // the chunks other channels took
+          if ((++spins & 1023u) == 0 && (long long)(globaltimer() - t0) > a.timeout_ns) {
+            atomicOr(a.err, 1ull + ((unsigned long long)kCounters << 8) + ((unsigned long long)me << 16));
+            ps.abort_ = 1;
+            break;
+          }
+        }
+      }
+      data_bar();
+      return true;
+    }
+  }
+  // after my own pipeline: take chunks of the rank's other channels' published C stages
+  __device__ void help_others() {
+    if constexpr (Op::kSteal) {
+      const int tid = (int)threadIdx.x - g_dbase;
+      for (int kk = 1; kk < a.nch; kk++) {
+        const int v = (ch + kk) % a.nch;
+        uint64_t* sw = chan_flags(a, me, v) + (size_t)kCounters * kLineWords;
+        for (;;) {
+          if (tid == 0) {
+            const uint64_t w = ld_acquire_gpu(sw);
+            const bool open = (w & 0xffffffull) < ((w >> 24) & 0xffffffull);
+            g_claim = sw;
+            g_claim_mode = open ? 2 : 0;
+            g_claim_tag = w & kTagMask;
+            g_claimed = 0;
+            g_vec_only = 1;
+          }
+          data_bar();
+          if (!g_claim_mode) break;
+          const uint64_t tag = g_claim_tag;
+          Op vop(a, blockIdx.y, v);
+          const size_t tv = (size_t)v + (size_t)(tag >> 52) * a.nch;
+          vop.stage(2, tv, (int)((tag >> 48) & 15u));  // vector part of the victim's C through my ring
+          data_bar();
+          if (tid == 0) {
+            g_claim_mode = 0;
+            g_vec_only = 0;
+            if (g_claimed) {
+              fence_acq_rel(a.gpu_scope);  // my stores (peers' y included) before the owner's acquire
+              red_add_relaxed(sw + 1, g_claimed, 1);
+            }
+          }
+          data_bar();
+        }
+      }
+      if (tid == 0) {
+        g_claim_mode = 0;
+        g_vec_only = 0;
+      }
+    }
+  }
   __device__ void work(long long it) {
     for (int p = 0; p < npos; p++) {
       long long tl;
       if (stage_at[p] < 0 || !tile_at(it, p, tl)) continue;
+      if (a.steal && stage_at[p] == 2 &&
+          owner_c((size_t)ch + (size_t)tl * a.nch, (int)((tiles0 + tl) % (unsigned long long)a.nslots), tl)) {
+        if (trc && threadIdx.x == 0 && it < a.trace_iters) trc[it * kTraceWords + 4 + 2] = globaltimer();
+        continue;
+      }
       op.stage(stage_at[p], (size_t)ch + (size_t)tl * a.nch, (int)((tiles0 + tl) % (unsigned long long)a.nslots));
       if (trc && threadIdx.x == 0 && it < a.trace_iters && stage_at[p] < 4)
         trc[it * kTraceWords + 4 + stage_at[p]] = globaltimer();
@@ -1109,6 +1339,8 @@ __device__ __forceinline__ void run_pipeline(const OpArgs& a, Op& op, int me, in
     ps.base[threadIdx.x / kMaxRanks][threadIdx.x % kMaxRanks] = B[threadIdx.x / kMaxRanks * kLineWords + threadIdx.x % kMaxRanks];
   tma_init(a.tma, (a.ws >= 2 ? (int)blockDim.x - 32 : (int)blockDim.x) / 32, a.l2hint);
   if (threadIdx.x == 0) {
+    g_claim_mode = 0;
+    g_vec_only = 0;
     ps.tiles0 = B[kCounters * kLineWords];
     ps.abort_ = 0;
     g_pf = !a.remote_pull;
@@ -1198,6 +1430,9 @@ __device__ __forceinline__ void run_pipeline(const OpArgs& a, Op& op, int me, in
       }
     }
   }
+  // ---- help the rank's other channels with their published C stages (HETCCL_STEAL) ----
+  if (a.steal && !*(volatile int*)&ps.abort_ && !(ws && sync_warp)) P.help_others();
+  __syncthreads();
   // ---- final stage (direct All-Reduce's E): one wait for every tile's signal instead of a position ----
   if (a.final_stage >= 0 && ((a.active >> a.final_stage) & 1u) && threadIdx.x < 32 && P.lane < P.n &&
       !*(volatile int*)&ps.abort_) {
@@ -1282,6 +1517,45 @@ struct ArOp {
     const int q = tp.rank_dom[o];
     return g.seg(tp.rank_idx[o] * (L / tp.dom_size[q]));
   }
+  // stage C on elements [c0, c1) of my piece of segment sg (any sub-range of the piece: every operand and
+  // destination address is linear in the element offset)
+  __device__ void fold_c(const Geo& g, int sg, size_t tb, size_t c0, size_t c1, int slot, size_t r0, T* my_s2) {
+    PtrList inner, outer, dst;
+    for (int i = 0; i < d; i++) inner.add(i == j ? (const void*)(x + tb + c0) : dsrc(i, slot, tb, c0, r0));
+    for (int q = 0; q < D; q++) {
+      if (q == k) outer.add(nullptr);
+      else outer.add_keep(my_s2 + (size_t)q * Rk + (c0 - r0));  // dead after this read
+    }
+    dst.add(y + tb + c0);
+    for (int q = 0; q < D; q++) {
+      if (q == k) continue;
+      const int o = owner_of(tp, q, sg);
+      const int dq = tp.dom_size[q];
+      if (a.flat_ag) {  // every member of domain q, not only the segment's owner (no forwarding stage D)
+        for (int i = 0; i < dq; i++) dst.add((T*)a.peer_recv[tp.members[tp.dom_first[q] + i]] + tb + c0);
+        continue;
+      }
+      if (a.direct) dst.add((T*)a.peer_recv[o] + tb + c0);  // straight into the owner's recv buffer
+      else dst.add(slot_ptr<T>(a, o, ch, slot) + s2_off(dq) + (size_t)D * (TL / dq) + (c0 - region_lo(g, o)));
+    }
+    for (int i = 0; i < d; i++)
+      if (i != j) {
+        if (a.direct) dst.add((T*)a.peer_recv[peer(i)] + tb + c0);
+        else
+          dst.add(slot_ptr<T>(a, peer(i), ch, slot) + s2_off(d) + (size_t)(D + 1) * Rk + (size_t)cidx(j, i) * Rk +
+                  (c0 - r0));
+      }
+    cta_fold_hier<T, OP>(inner, k, outer, dst, c1 - c0);
+  }
+  // number of non-empty pieces of my C stage in tile t (chunk stealing needs exactly one)
+  __device__ int c_pieces(size_t t) const {
+    const size_t tb = t * TL, len = min(TL, a.count - tb);
+    const Geo g{len, TL, L, D};
+    int np = 0;
+    for (int sg = s_lo; sg < s_hi; sg++) np += g.piece(sg, k + 1) > g.piece(sg, k);
+    return np;
+  }
+  static constexpr bool kSteal = true;  // stage 2 can be split into units other channels may take
   __device__ void stage(int s, size_t t, int slot) {
     const size_t tb = t * TL, len = min(TL, a.count - tb);
     const Geo g{len, TL, L, D};
@@ -1318,33 +1592,7 @@ struct ArOp {
     } else if (s == 2) {  // ---- C: P_k of my pieces (domain fold) + the other partials; final -> y, owners, peers ----
       for (int sg = s_lo; sg < s_hi; sg++) {
         const size_t c0 = g.piece(sg, k), c1 = g.piece(sg, k + 1);
-        if (c1 <= c0) continue;
-        PtrList inner, outer, dst;
-        for (int i = 0; i < d; i++) inner.add(i == j ? (const void*)(x + tb + c0) : dsrc(i, slot, tb, c0, r0));
-        for (int q = 0; q < D; q++) {
-          if (q == k) outer.add(nullptr);
-          else outer.add_keep(my_s2 + (size_t)q * Rk + (c0 - r0));  // dead after this read
-        }
-        dst.add(y + tb + c0);
-        for (int q = 0; q < D; q++) {
-          if (q == k) continue;
-          const int o = owner_of(tp, q, sg);
-          const int dq = tp.dom_size[q];
-          if (a.flat_ag) {  // every member of domain q, not only the segment's owner (no forwarding stage D)
-            for (int i = 0; i < dq; i++) dst.add((T*)a.peer_recv[tp.members[tp.dom_first[q] + i]] + tb + c0);
-            continue;
-          }
-          if (a.direct) dst.add((T*)a.peer_recv[o] + tb + c0);  // straight into the owner's recv buffer
-          else dst.add(slot_ptr<T>(a, o, ch, slot) + s2_off(dq) + (size_t)D * (TL / dq) + (c0 - region_lo(g, o)));
-        }
-        for (int i = 0; i < d; i++)
-          if (i != j) {
-            if (a.direct) dst.add((T*)a.peer_recv[peer(i)] + tb + c0);
-            else
-              dst.add(slot_ptr<T>(a, peer(i), ch, slot) + s2_off(d) + (size_t)(D + 1) * Rk + (size_t)cidx(j, i) * Rk +
-                      (c0 - r0));
-          }
-        cta_fold_hier<T, OP>(inner, k, outer, dst, c1 - c0);
+        if (c1 > c0) fold_c(g, sg, tb, c0, c1, slot, r0, my_s2);
       }
     } else if (s == 3 && a.direct) {  // ---- D (direct): forward the other owners' pieces (now in y) to peers ----
       PtrList peers_y;
@@ -1405,6 +1653,7 @@ struct ArOp {
 //         2 C domain fold of my shard + cross fold -> y
 template <typename T, int OP>
 struct RsOp {
+  static constexpr bool kSteal = false;
   static constexpr int ES = sizeof(T);
   static constexpr int V = Tr<T>::V;
   const OpArgs& a;
@@ -1486,6 +1735,7 @@ struct RsOp {
 // Stages: 0 A cross push | 1 B own shard + received pieces -> y and domain peers | 2 C peers -> y
 template <typename T>
 struct AgOp {
+  static constexpr bool kSteal = false;
   static constexpr int ES = sizeof(T);
   static constexpr int V = 16 / ES;
   const OpArgs& a;
@@ -1568,6 +1818,7 @@ struct AgOp {
 // Stages: 0 A root scatter | 1 B cross push | 2 C region -> y and domain peers | 3 D peers -> y
 template <typename T>
 struct BcOp {
+  static constexpr bool kSteal = false;
   static constexpr int ES = sizeof(T);
   static constexpr int V = 16 / ES;
   const OpArgs& a;
@@ -1680,6 +1931,7 @@ struct BcOp {
 // everyone's pieces into y. Slot layout on a rank of domain k: s1[d-1][Rk] | s2[D][Rk] | fin[T] (root).
 template <typename T, int OP>
 struct RdOp {
+  static constexpr bool kSteal = false;
   static constexpr int ES = sizeof(T);
   const OpArgs& a;
   const Topo& tp;
@@ -1777,6 +2029,7 @@ struct RdOp {
 // domain). Slot layout: in[n-1][T] (compact sender index). Stages: 0 A push blocks | 1 B copy-out.
 template <typename T>
 struct A2aOp {
+  static constexpr bool kSteal = false;
   static constexpr int ES = sizeof(T);
   const OpArgs& a;
   int me, ch, n;
