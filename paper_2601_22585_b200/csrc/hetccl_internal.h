@@ -130,6 +130,7 @@ struct OpArgs {
   int l2hint;                   // 1: L2 policies in the TMA movers (evict_first streams, evict_last + discard partials)
   int spacing;                  // plain pipeline (ws == 0): positions between consecutive stages (1 = adjacent)
   int steal;                    // 1: All-Reduce C stages are published as units other channels of the rank may take
+  int s2g;                      // 1: the TMA movers store results with bulk copies shared -> global
 };
 
 // ---- host plan (plan.cpp) ----

@@ -333,15 +333,24 @@ __device__ __forceinline__ void st_v4_hint(void* p, const uint4& v, uint64_t pol
 __device__ __forceinline__ void discard_l2(const void* p) {
   asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
 }
+__device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_addr(ssrc)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __shared__ int g_l2hint;  // OpArgs::l2hint of the running op
+__shared__ int g_s2g;     // 1: the ring movers store results by TMA bulk copies shared -> global (OpArgs::s2g)
 __shared__ uint32_t g_keep_dst, g_dead_ops;  // the current call's hint masks (destinations / operands)
 __device__ __forceinline__ void data_bar() { asm volatile("bar.sync 1, %0;" ::"r"(g_dnth) : "memory"); }
 
 // thread 0 at the start of a pipeline kernel, before its first __syncthreads (data warps: all warps, or
 // all but the sync warp in the warp-specialised mode)
-__device__ __forceinline__ void tma_init(int enable, int data_warps, int l2hint) {
+__device__ __forceinline__ void tma_init(int enable, int data_warps, int l2hint, int s2g) {
   if (threadIdx.x == 0) {
     g_tma = HETCCL_TMA && !HETCCL_LEGACY_MOVERS && enable;
+    g_s2g = s2g;
     g_lgsts = HETCCL_LEGACY_MOVERS;
     g_l2hint = l2hint;
     g_seq = 0;
@@ -386,9 +395,15 @@ __device__ __noinline__ void tma_stream(int ni, int D, int kpos, int nd, uint32_
   const int hint = g_l2hint & 3;
   const uint32_t keep = (g_l2hint & 2) ? g_keep_dst : 0u, dead = (g_l2hint & 4) ? g_dead_ops : 0u;
   const uint64_t pol_first = policy_evict_first(), pol_last = policy_evict_last();
+  // S2G (HETCCL_S2G): each result vector goes back into operand 0's slot of the stage, and one thread stores the
+  // chunk to every destination with bulk copies — one instruction per destination instead of one 16-byte store
+  // per thread and vector, which is what limits a CTA pushing to NVLink peers (tools/tma_probe.cu: one TMA
+  // thread per CTA pushes ~43 GB/s, r02v)
+  const int s2g = g_s2g;
   auto issue = [&](uint32_t cn) {
     const unsigned g = seq0 + cn, st = g % kTmaStages, u = g / kTmaStages;
     if (u > 0) mbar_wait(&g_empty[st], (u - 1) & 1u);  // every data warp is done with the stage's last use
+    if (s2g && u > 0) bulk_wait_read();                 // ... and my bulk stores have read it
     const uint32_t bytes = min(cv, nv - cn * cv) * 16;
     mbar_arrive_expect_tx(&g_full[st], bytes * (uint32_t)nops);
     for (int j = 0; j < nops; j++) {
@@ -445,7 +460,9 @@ __device__ __noinline__ void tma_stream(int ni, int D, int kpos, int nd, uint32_
         for (int e = 0; e < V; e++) Vec<S>::set(o, e, TR::narrow(acc[e]));
       }
       const size_t off = ((size_t)c * cv + idx) * 16;
-      if (hint == 3) {
+      if (s2g) {
+        *(uint4*)(sb + idx * 16) = o;  // operand 0's slot: only this thread read it
+      } else if (hint == 3) {
         for (int d = 0; d < nd; d++) st_v4_hint(g_dst[d] + off, o, ((keep >> d) & 1u) ? pol_last : pol_first);
       } else if (hint == 2) {
         for (int d = 0; d < nd; d++) {
@@ -458,9 +475,18 @@ __device__ __noinline__ void tma_stream(int ni, int D, int kpos, int nd, uint32_
         for (int d = 0; d < nd; d++) st_v4(g_dst[d] + off, o);
       }
     }
+    if (s2g) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // my smem results -> the bulk copy engine
+      data_bar();
+      if (tid == 0) {
+        for (int d = 0; d < nd; d++) bulk_s2g(g_dst[d] + (size_t)c * chb, sb, lim * 16);
+        bulk_commit();
+      }
+    }
     __syncwarp();
     if (lane == 0) mbar_arrive(&g_empty[st]);  // this warp is done with stage st
   }
+  if (s2g && tid == 0) bulk_wait_all();  // the stores are complete (visible) before the pipeline's release fence
   *(volatile unsigned*)&g_seq = seq0 + nchunks;  // every data thread writes the same value
 }
 
@@ -1337,7 +1363,7 @@ __device__ __forceinline__ void run_pipeline(const OpArgs& a, Op& op, int me, in
   P.npos = P.SP * (P.np - 1) + 1;
   if (threadIdx.x < kCounters * kMaxRanks)
     ps.base[threadIdx.x / kMaxRanks][threadIdx.x % kMaxRanks] = B[threadIdx.x / kMaxRanks * kLineWords + threadIdx.x % kMaxRanks];
-  tma_init(a.tma, (a.ws >= 2 ? (int)blockDim.x - 32 : (int)blockDim.x) / 32, a.l2hint);
+  tma_init(a.tma, (a.ws >= 2 ? (int)blockDim.x - 32 : (int)blockDim.x) / 32, a.l2hint, a.s2g);
   if (threadIdx.x == 0) {
     g_claim_mode = 0;
     g_vec_only = 0;

@@ -333,6 +333,9 @@ hetcclResult_t run_op(hetcclComm_t c, int op, const void* const* sends, void* co
   // chunk stealing of C stages (opt-in: it evens the channels' finish times, 60-100 us spread instead of 150-270,
   // but the claims cost more than the tail they remove: r02an/r02ao mux 503-505 -> 473-476 GB/s)
   a.steal = op == OP_ALLREDUCE && env_long("HETCCL_STEAL", 0) != 0;
+  // results leave the TMA movers as bulk copies shared -> global (r02at: mux 501 -> 517 GB/s; across GPUs on the
+  // TMA kernels 2+2 at 148 channels 513 -> 530, 1+1 376 -> 446)
+  a.s2g = (int)env_long("HETCCL_S2G", 1);
   a.l2hint = (int)env_long("HETCCL_L2HINT", 1);  // evict_first streams (r02n: +4%; partial keep/discard bits 2/4 lose)
   // direct recv mode: in a rank-multiplexed comm every rank's recv buffer is a local pointer; with one
   // rank per GPU, when recvbuf lies in a connected symmetric buffer (hetccl_mem_*), at the same offset in
