@@ -337,6 +337,11 @@ __device__ __forceinline__ void bulk_s2g(void* gdst, const void* ssrc, uint32_t 
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_addr(ssrc)), "r"(bytes)
                : "memory");
 }
+__device__ __forceinline__ void bulk_s2g_hint(void* gdst, const void* ssrc, uint32_t bytes, uint64_t pol) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(gdst),
+               "r"(smem_addr(ssrc)), "r"(bytes), "l"(pol)
+               : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
@@ -479,7 +484,10 @@ __device__ __noinline__ void tma_stream(int ni, int D, int kpos, int nd, uint32_
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // my smem results -> the bulk copy engine
       data_bar();
       if (tid == 0) {
-        for (int d = 0; d < nd; d++) bulk_s2g(g_dst[d] + (size_t)c * chb, sb, lim * 16);
+        for (int d = 0; d < nd; d++) {
+          if (hint & 1) bulk_s2g_hint(g_dst[d] + (size_t)c * chb, sb, lim * 16, ((keep >> d) & 1u) ? pol_last : pol_first);
+          else bulk_s2g(g_dst[d] + (size_t)c * chb, sb, lim * 16);
+        }
         bulk_commit();
       }
     }

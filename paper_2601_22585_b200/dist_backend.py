@@ -16,6 +16,7 @@ all_gather(_into_tensor), reduce_scatter(_tensor), all_to_all_single with equal 
 int32 / fp32 / bf16 / fp16. Anything else raises.
 """
 import os
+import time
 
 import torch
 import torch.distributed as dist
@@ -94,8 +95,11 @@ class ProcessGroupHetccl(dist.ProcessGroup):
         # others spinning in their first collective)
         store.add("hetccl/failed", 1 - ok)
         store.add("hetccl/arrived", 1)
+        limit = time.monotonic() + (timeout.total_seconds() if timeout is not None else 1800.0)
         while store.add("hetccl/arrived", 0) < size:
-            pass
+            if time.monotonic() > limit:
+                raise HetcclError(2, "hetccl backend: timed out waiting for every rank to connect")
+            time.sleep(0.001)
         if store.add("hetccl/failed", 0):
             hetccl_comm_destroy(self.comm)
             self.comm = None
