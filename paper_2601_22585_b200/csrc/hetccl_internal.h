@@ -160,5 +160,17 @@ void nvls_destroy(NvlsState* s);
 void nvls_buffer(const NvlsState* s, void** p, size_t* bytes);
 int nvls_supports(const NvlsState* s, int dt, int red, const void* send, const void* recv);
 int nvls_aliases_staging(const NvlsState* s, int dt, const void* p, size_t bytes);
+// one rank per process: NVLS state begun at comm init (the domain leader creates the multicast object and a
+// socket that hands its file descriptor to the members), finished at connect (handle passing, every member's
+// device added, memory bound, peers' cross slots / flags opened through CUDA IPC)
+struct NvlsBlob {
+  int enabled;         // this rank began NVLS set-up
+  char sock[44];       // domain leader: abstract unix-socket name (no leading NUL), else empty
+  char ipc[64];        // cudaIpcMemHandle_t of this rank's cross slots + flags
+};
+int nvls_proc_begin(const Topo& t, int rank, int dev, size_t bytes_per_rank, int nch, NvlsState** out, NvlsBlob* blob,
+                    char* err, size_t errlen);
+int nvls_proc_connect(NvlsState* s, const Topo& t, int rank, const NvlsBlob* const* blobs, long long timeout_ns,
+                      char* err, size_t errlen);
 
 }  // namespace hetccl

@@ -26,6 +26,13 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <errno.h>
+#include <poll.h>
+#include <sys/socket.h>
+#include <sys/un.h>
+#include <time.h>
+#include <unistd.h>
+
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
@@ -361,6 +368,8 @@ struct Drv {
   NV_FN(cuMemUnmap);
   NV_FN(cuMemSetAccess);
   NV_FN(cuMemGetAllocationGranularity);
+  NV_FN(cuMemExportToShareableHandle);
+  NV_FN(cuMemImportFromShareableHandle);
   bool ok = false;
 };
 #undef NV_FN
@@ -392,6 +401,8 @@ Drv& drv() {
   NV_GET(cuMemUnmap);
   NV_GET(cuMemSetAccess);
   NV_GET(cuMemGetAllocationGranularity);
+  NV_GET(cuMemExportToShareableHandle);
+  NV_GET(cuMemImportFromShareableHandle);
 #undef NV_GET
   d.ok = ok;
   return d;
@@ -415,6 +426,15 @@ struct NvlsState {
   McShared* mcs = nullptr;
   char* xs = nullptr;        // cross slots [2][D][ce/d] (cudaMalloc)
   uint64_t* fl = nullptr;    // flags [nch][4][kMaxRanks] + base[nch] (cudaMalloc, zeroed)
+  // one rank per process (nvls_proc_*): the domain leader's listening socket and exported multicast handle,
+  // and the peers' xs / fl as opened through CUDA IPC
+  int listen_fd = -1, mc_fd = -1;
+  bool mc_imported = false;
+  char* peer_xs[kMaxRanks] = {nullptr};
+  uint64_t* peer_fl[kMaxRanks] = {nullptr};
+  bool peer_ipc[kMaxRanks] = {false};
+  bool joint = false;        // xs and fl are one allocation (one-rank-per-process set-up)
+  size_t gran = 0;
   NvlsArgs tmpl{};           // peers, topology (pointers filled at create)
 };
 
@@ -455,8 +475,14 @@ void nvls_destroy(NvlsState* s) {
     if (s->mcs->h) D.p_cuMemRelease(s->mcs->h);
     delete s->mcs;
   }
+  for (int r = 0; r < kMaxRanks; r++) {
+    if (!s->peer_ipc[r]) continue;
+    if (s->peer_xs[r]) cudaIpcCloseMemHandle(s->peer_xs[r]);
+  }
   if (s->xs) cudaFree(s->xs);
-  if (s->fl) cudaFree(s->fl);
+  if (s->fl && !s->joint) cudaFree(s->fl);
+  if (s->listen_fd >= 0) close(s->listen_fd);
+  if (s->mc_fd >= 0) close(s->mc_fd);
   cudaSetDevice(prev);
   delete s;
 }
@@ -603,6 +629,266 @@ int nvls_aliases_staging(const NvlsState* s, int dt, const void* p, size_t bytes
   if (!s || !s->wide || dtype_size(dt) != 2 || !p) return 0;
   const uintptr_t a0 = (uintptr_t)p, u0 = (uintptr_t)s->uc;
   return a0 < u0 + s->bytes && u0 < a0 + bytes;
+}
+
+// ---------------------------------------------------------------- one rank per process ----------
+namespace {
+long long now_ns() {
+  timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return (long long)ts.tv_sec * 1000000000LL + ts.tv_nsec;
+}
+// wait until fd is readable (or writable), at most until the deadline
+bool wait_fd(int fd, short ev, long long deadline) {
+  for (;;) {
+    const long long left = deadline - now_ns();
+    if (left <= 0) return false;
+    pollfd p{fd, ev, 0};
+    const int r = poll(&p, 1, (int)std::min<long long>(left / 1000000 + 1, 1000));
+    if (r > 0) return true;
+    if (r < 0) return false;
+  }
+}
+bool send_byte(int fd, char c, int pass_fd = -1) {
+  iovec io{&c, 1};
+  msghdr m{};
+  m.msg_iov = &io;
+  m.msg_iovlen = 1;
+  char ctl[CMSG_SPACE(sizeof(int))];
+  if (pass_fd >= 0) {
+    memset(ctl, 0, sizeof(ctl));
+    m.msg_control = ctl;
+    m.msg_controllen = sizeof(ctl);
+    cmsghdr* cm = CMSG_FIRSTHDR(&m);
+    cm->cmsg_level = SOL_SOCKET;
+    cm->cmsg_type = SCM_RIGHTS;
+    cm->cmsg_len = CMSG_LEN(sizeof(int));
+    memcpy(CMSG_DATA(cm), &pass_fd, sizeof(int));
+  }
+  return sendmsg(fd, &m, 0) == 1;
+}
+// receive one byte (and a passed file descriptor, if any) before the deadline
+bool recv_byte(int fd, char want, long long deadline, int* got_fd = nullptr) {
+  if (!wait_fd(fd, POLLIN, deadline)) return false;
+  char c = 0;
+  iovec io{&c, 1};
+  msghdr m{};
+  m.msg_iov = &io;
+  m.msg_iovlen = 1;
+  char ctl[CMSG_SPACE(sizeof(int))];
+  memset(ctl, 0, sizeof(ctl));
+  m.msg_control = ctl;
+  m.msg_controllen = sizeof(ctl);
+  if (recvmsg(fd, &m, 0) != 1 || c != want) return false;
+  if (got_fd) {
+    cmsghdr* cm = CMSG_FIRSTHDR(&m);
+    if (!cm || cm->cmsg_type != SCM_RIGHTS) return false;
+    memcpy(got_fd, CMSG_DATA(cm), sizeof(int));
+  }
+  return true;
+}
+sockaddr_un abstract_addr(const char* name, socklen_t* len) {
+  sockaddr_un a{};
+  a.sun_family = AF_UNIX;
+  a.sun_path[0] = 0;  // abstract namespace: no file, gone with the socket
+  strncpy(a.sun_path + 1, name, sizeof(a.sun_path) - 2);
+  *len = (socklen_t)(offsetof(sockaddr_un, sun_path) + 1 + strlen(name));
+  return a;
+}
+// uc: this device's memory bound to the multicast object, mapped at uc; mc: the multicast address
+int bind_and_map(NvlsState* s, char* err, size_t errlen) {
+  Drv& D = drv();
+  CUmemAllocationProp p{};
+  p.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  p.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  p.location.id = s->dev;
+  p.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  int rc;
+  if ((rc = D.p_cuMemCreate(&s->uc_h, s->bytes, &p, 0))) return nv_err(err, errlen, "cuMemCreate", rc), 1;
+  if ((rc = D.p_cuMulticastBindMem(s->mcs->h, 0, s->uc_h, 0, s->bytes, 0)))
+    return nv_err(err, errlen, "cuMulticastBindMem", rc), 1;
+  CUmemAccessDesc acc{};
+  acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  acc.location.id = s->dev;
+  acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  if ((rc = D.p_cuMemAddressReserve(&s->uc, s->bytes, s->gran, 0, 0))) return nv_err(err, errlen, "reserve(uc)", rc), 1;
+  if ((rc = D.p_cuMemMap(s->uc, s->bytes, 0, s->uc_h, 0))) return nv_err(err, errlen, "cuMemMap(uc)", rc), 1;
+  if ((rc = D.p_cuMemSetAccess(s->uc, s->bytes, &acc, 1))) return nv_err(err, errlen, "cuMemSetAccess(uc)", rc), 1;
+  if ((rc = D.p_cuMemAddressReserve(&s->mc, s->bytes, s->gran, 0, 0))) return nv_err(err, errlen, "reserve(mc)", rc), 1;
+  if ((rc = D.p_cuMemMap(s->mc, s->bytes, 0, s->mcs->h, 0))) return nv_err(err, errlen, "cuMemMap(mc)", rc), 1;
+  if ((rc = D.p_cuMemSetAccess(s->mc, s->bytes, &acc, 1))) return nv_err(err, errlen, "cuMemSetAccess(mc)", rc), 1;
+  if (cudaMemset((void*)s->uc, 0, s->bytes) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess)
+    return nv_err(err, errlen, "cudaMemset(uc)", 0), 1;
+  return 0;
+}
+}  // namespace
+
+int nvls_proc_begin(const Topo& t, int rank, int dev, size_t bytes_per_rank, int nch, NvlsState** out, NvlsBlob* blob,
+                    char* err, size_t errlen) {
+  *out = nullptr;
+  memset(blob, 0, sizeof(*blob));
+  if (!nvls_eligible_topo(t)) return nv_err(err, errlen, "domain sizes must be equal and >= 2", 0), 1;
+  Drv& D = drv();
+  if (!D.ok) return nv_err(err, errlen, "driver entry points", 0), 1;
+  const int d = t.dom_size[0];
+  CUdevice cd;
+  int sup = 0;
+  if (D.p_cuDeviceGet(&cd, dev) != CUDA_SUCCESS ||
+      D.p_cuDeviceGetAttribute(&sup, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, cd) != CUDA_SUCCESS || !sup)
+    return nv_err(err, errlen, "multicast not supported on this device", dev), 1;
+  CUmulticastObjectProp mp{};
+  mp.numDevices = (unsigned)d;
+  mp.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  mp.size = bytes_per_rank;
+  size_t mg = 0, ag = 0;
+  CUmemAllocationProp ap{};
+  ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  ap.location.id = dev;
+  ap.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+  int rc;
+  if ((rc = D.p_cuMulticastGetGranularity(&mg, &mp, CU_MULTICAST_GRANULARITY_MINIMUM)) ||
+      (rc = D.p_cuMemGetAllocationGranularity(&ag, &ap, CU_MEM_ALLOC_GRANULARITY_MINIMUM)))
+    return nv_err(err, errlen, "granularity", rc), 1;
+  NvlsState* s = new NvlsState();
+  s->dev = dev;
+  s->rank = rank;
+  s->nch = nch;
+  s->gran = std::max(mg, ag);
+  s->bytes = (std::max(bytes_per_rank, (size_t)1) + s->gran - 1) / s->gran * s->gran;
+  s->ce_bytes = s->bytes / ((size_t)16 * d) * ((size_t)16 * d);
+  const char* w = getenv("HETCCL_NVLS_WIDE");
+  s->wide = !(w && *w == '0');
+  s->joint = true;
+  const size_t xs_bytes = (2 * (size_t)t.D * (s->ce_bytes / d) + 255) / 256 * 256;
+  const size_t flb = ((size_t)nch * kNvCounters * kMaxRanks + nch) * sizeof(uint64_t);
+  auto fail = [&](const char* what, int code) {
+    nv_err(err, errlen, what, code);
+    nvls_destroy(s);
+    return 1;
+  };
+  if (cudaMalloc((void**)&s->xs, xs_bytes + flb) != cudaSuccess) return fail("cudaMalloc(xs, flags)", 0);
+  s->fl = (uint64_t*)(s->xs + xs_bytes);
+  if (cudaMemset(s->fl, 0, flb) != cudaSuccess || cudaDeviceSynchronize() != cudaSuccess) return fail("cudaMemset", 0);
+  cudaIpcMemHandle_t h;
+  if (cudaIpcGetMemHandle(&h, s->xs) != cudaSuccess) return fail("cudaIpcGetMemHandle(xs)", 0);
+  memcpy(blob->ipc, &h, sizeof(h));
+  s->tmpl.xs_slot = s->ce_bytes / d;
+  if (t.rank_idx[rank] == 0) {  // domain leader: the multicast object and the socket that hands it out
+    s->mcs = new McShared();
+    s->mcs->refs = 1;
+    mp.size = s->bytes;
+    if ((rc = D.p_cuMulticastCreate(&s->mcs->h, &mp))) return fail("cuMulticastCreate", rc);
+    if ((rc = D.p_cuMulticastAddDevice(s->mcs->h, cd))) return fail("cuMulticastAddDevice", rc);
+    if ((rc = D.p_cuMemExportToShareableHandle(&s->mc_fd, s->mcs->h, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0)))
+      return fail("cuMemExportToShareableHandle", rc);
+    snprintf(blob->sock, sizeof(blob->sock), "hetccl-nvls-%d-%d-%llx", (int)getpid(), rank,
+             (unsigned long long)now_ns());
+    s->listen_fd = socket(AF_UNIX, SOCK_STREAM | SOCK_CLOEXEC, 0);
+    socklen_t len;
+    sockaddr_un a = abstract_addr(blob->sock, &len);
+    if (s->listen_fd < 0 || bind(s->listen_fd, (sockaddr*)&a, len) != 0 || listen(s->listen_fd, kMaxRanks) != 0)
+      return fail("leader socket", errno);
+  }
+  blob->enabled = 1;
+  *out = s;
+  return 0;
+}
+
+int nvls_proc_connect(NvlsState* s, const Topo& t, int rank, const NvlsBlob* const* blobs, long long timeout_ns,
+                      char* err, size_t errlen) {
+  Drv& D = drv();
+  const long long deadline = now_ns() + timeout_ns;
+  const int k = t.rank_dom[rank], d = t.dom_size[k];
+  const int leader = t.members[t.dom_first[k]];
+  CUdevice cd;
+  D.p_cuDeviceGet(&cd, s->dev);
+  // every peer's cross slots + flags
+  const size_t xs_bytes = (size_t)((char*)s->fl - s->xs);
+  for (int r = 0; r < t.n; r++) {
+    if (r == rank) continue;
+    cudaIpcMemHandle_t h;
+    memcpy(&h, blobs[r]->ipc, sizeof(h));
+    void* p = nullptr;
+    if (cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess)
+      return nv_err(err, errlen, "cudaIpcOpenMemHandle(nvls)", r), 1;
+    s->peer_xs[r] = (char*)p;
+    s->peer_fl[r] = (uint64_t*)((char*)p + xs_bytes);
+    s->peer_ipc[r] = true;
+  }
+  if (rank == leader) {
+    // hand the multicast handle to every member, wait until each added its device, then everyone binds
+    int conns[kMaxRanks];
+    int nc = 0;
+    bool ok = true;
+    for (; nc < d - 1 && ok; nc++) {
+      ok = wait_fd(s->listen_fd, POLLIN, deadline);
+      conns[nc] = ok ? accept4(s->listen_fd, nullptr, nullptr, SOCK_CLOEXEC) : -1;
+      ok = ok && conns[nc] >= 0 && send_byte(conns[nc], 'F', s->mc_fd);
+    }
+    for (int i = 0; i < nc && ok; i++) ok = recv_byte(conns[i], 'A', deadline);
+    for (int i = 0; i < nc && ok; i++) ok = send_byte(conns[i], 'B');
+    ok = ok && bind_and_map(s, err, errlen) == 0;
+    for (int i = 0; i < nc && ok; i++) ok = recv_byte(conns[i], 'C', deadline);
+    for (int i = 0; i < nc && ok; i++) ok = send_byte(conns[i], 'D');
+    for (int i = 0; i < nc; i++)
+      if (conns[i] >= 0) close(conns[i]);
+    if (!ok) return (err && !*err ? nv_err(err, errlen, "leader hand-off", 0) : (void)0), 1;
+  } else {
+    if (!blobs[leader]->sock[0]) return nv_err(err, errlen, "leader published no socket", leader), 1;
+    socklen_t len;
+    sockaddr_un a = abstract_addr(blobs[leader]->sock, &len);
+    int fd = -1;
+    while (fd < 0) {
+      fd = socket(AF_UNIX, SOCK_STREAM | SOCK_CLOEXEC, 0);
+      if (fd >= 0 && connect(fd, (sockaddr*)&a, len) == 0) break;
+      if (fd >= 0) close(fd);
+      fd = -1;
+      if (now_ns() > deadline) return nv_err(err, errlen, "connect to leader", errno), 1;
+      usleep(1000);
+    }
+    int mfd = -1;
+    bool ok = recv_byte(fd, 'F', deadline, &mfd);
+    if (ok) {
+      s->mcs = new McShared();
+      s->mcs->refs = 1;
+      int rc = D.p_cuMemImportFromShareableHandle(&s->mcs->h, (void*)(uintptr_t)mfd,
+                                                  CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR);
+      close(mfd);
+      ok = rc == CUDA_SUCCESS && D.p_cuMulticastAddDevice(s->mcs->h, cd) == CUDA_SUCCESS;
+      if (!ok) nv_err(err, errlen, "import / add device", rc);
+    }
+    ok = ok && send_byte(fd, 'A') && recv_byte(fd, 'B', deadline);
+    ok = ok && bind_and_map(s, err, errlen) == 0;
+    ok = ok && send_byte(fd, 'C') && recv_byte(fd, 'D', deadline);
+    close(fd);
+    if (!ok) return (err && !*err ? nv_err(err, errlen, "member hand-off", 0) : (void)0), 1;
+  }
+  if (s->listen_fd >= 0) {
+    close(s->listen_fd);
+    s->listen_fd = -1;
+  }
+  // kernel arguments (as nvls_create's, with the peers' buffers as opened here)
+  NvlsArgs& a = s->tmpl;
+  const size_t xs_slot = a.xs_slot;
+  memset(&a, 0, sizeof(a));
+  a.me = rank;
+  a.d = d;
+  a.D = t.D;
+  a.i = t.rank_idx[rank];
+  a.k = k;
+  a.nch = s->nch;
+  a.xs_slot = xs_slot;
+  a.uc = (char*)s->uc;
+  a.mc = (char*)s->mc;
+  for (int j = 0; j < d; j++) a.dmem[j] = t.members[t.dom_first[k] + j];
+  for (int q = 0; q < t.D; q++) {
+    const int x = t.members[t.dom_first[q] + a.i];
+    a.xrank[q] = x;
+    a.xs[q] = x == rank ? s->xs : s->peer_xs[x];
+  }
+  for (int p = 0; p < t.n; p++) a.fl[p] = p == rank ? s->fl : s->peer_fl[p];
+  return 0;
 }
 
 void nvls_buffer(const NvlsState* s, void** p, size_t* bytes) {

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -71,7 +72,9 @@ struct hetcclComm {
     bool ipc[kMaxRanks] = {false};
   };
   std::vector<SymBuf> sym;
-  NvlsState* nvls = nullptr;              // HETCCL_NVLS=1 at hetccl_comm_init_all (nvls.cu), else null
+  NvlsState* nvls = nullptr;              // HETCCL_NVLS=1: per-domain multicast All-Reduce (nvls.cu), else null
+  NvlsState* nvls_pending = nullptr;      // one rank per process: begun at init, finished at connect
+  NvlsBlob nvls_blob{};
   std::string last_error;
 };
 
@@ -88,6 +91,7 @@ struct Blob {
   int nslots;
   unsigned long long os_bytes;
   cudaIpcMemHandle_t handle;
+  NvlsBlob nvls;
 };
 static_assert(sizeof(Blob) <= HETCCL_BLOB_BYTES, "blob too large");
 constexpr uint32_t kMagic = 0x48435431u;  // "HCT1"
@@ -493,6 +497,15 @@ hetcclResult_t hetccl_comm_init(hetcclComm_t* comm, int nranks, int rank, const 
   }
   c->mapped[rank] = c->local[0];
   if (nranks == 1) c->connected = true;
+  // HETCCL_NVLS=1 (opt-in, NEXT-1) with one rank per process: the domain leader creates the multicast object now;
+  // connect hands it to the members (hetccl_comm_nvls reports whether the comm ended up in NVLS mode)
+  if (nranks > 1 && env_long("HETCCL_NVLS", 0) == 1) {
+    char why[256] = {0};
+    const size_t mb = (size_t)std::max(1L, env_long("HETCCL_NVLS_MB", 32));
+    const int nch = (int)std::max(1L, std::min(1024L, env_long("HETCCL_NVLS_NCH", 148)));
+    if (nvls_proc_begin(c->topo, rank, cuda_device, mb << 20, nch, &c->nvls_pending, &c->nvls_blob, why, sizeof(why)))
+      c->last_error = why;
+  }
   *comm = c;
   return hetcclSuccess;
 }
@@ -513,6 +526,7 @@ hetcclResult_t hetccl_comm_export(hetcclComm_t c, void* blob, size_t* blob_bytes
   b.ws = c->ws;
   b.nslots = c->nslots;
   b.os_bytes = c->os_bytes;
+  b.nvls = c->nvls_blob;
   DevGuard g(c->device);
   CUDA_TRY(c, cudaIpcGetMemHandle(&b.handle, c->local[0]));
   memset(blob, 0, HETCCL_BLOB_BYTES);
@@ -546,6 +560,42 @@ hetcclResult_t hetccl_comm_connect(hetcclComm_t c, const void* blobs, size_t blo
     c->ipc_opened[r] = true;
   }
   c->connected = true;
+  // NVLS (one rank per process): only if every rank began it; then every rank must also finish it, agreed
+  // through a status word in each rank's region (1 ok, 2 failed) so no two ranks pick different paths
+  bool all_nvls = true;
+  const NvlsBlob* nb[kMaxRanks];
+  for (int r = 0; r < c->n; r++) {
+    nb[r] = &((const Blob*)((const char*)blobs + (size_t)r * HETCCL_BLOB_BYTES))->nvls;
+    all_nvls = all_nvls && nb[r]->enabled;
+  }
+  if (c->nvls_pending && all_nvls) {
+    char why[256] = {0};
+    const bool ok = nvls_proc_connect(c->nvls_pending, c->topo, c->rank, nb, c->timeout_ns, why, sizeof(why)) == 0;
+    if (!ok) c->last_error = why;
+    auto status = [&](int r) { return (uint64_t*)(c->mapped[r] + kFlagsReserve / 2) + (size_t)kCounters * kLineWords + 8; };
+    const uint64_t mine = ok ? 1 : 2;
+    bool agree = cudaMemcpy(status(c->rank), &mine, 8, cudaMemcpyHostToDevice) == cudaSuccess && ok;
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int r = 0; r < c->n && agree; r++) {
+      uint64_t v = 0;
+      while (v == 0) {
+        if (cudaMemcpy(&v, status(r), 8, cudaMemcpyDeviceToHost) != cudaSuccess) break;
+        if (v == 0 && std::chrono::steady_clock::now() - t0 > std::chrono::nanoseconds(c->timeout_ns)) break;
+        if (v == 0) usleep(1000);
+      }
+      agree = v == 1;
+    }
+    if (agree) {
+      c->nvls = c->nvls_pending;
+    } else {
+      nvls_destroy(c->nvls_pending);
+      if (c->last_error.empty()) c->last_error = "NVLS: a rank could not finish the set-up; staying on the P2P path";
+    }
+    c->nvls_pending = nullptr;
+  } else if (c->nvls_pending) {
+    nvls_destroy(c->nvls_pending);
+    c->nvls_pending = nullptr;
+  }
   return hetcclSuccess;
 }
 
@@ -670,6 +720,7 @@ hetcclResult_t hetccl_comm_init_mux(hetcclComm_t* comm, int nranks, const int* r
 hetcclResult_t hetccl_comm_destroy(hetcclComm_t c) {
   if (!c) return hetcclInvalidArgument;
   if (c->nvls) nvls_destroy(c->nvls);
+  if (c->nvls_pending) nvls_destroy(c->nvls_pending);
   {
     DevGuard g(c->device);
     cudaDeviceSynchronize();

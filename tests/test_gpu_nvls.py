@@ -181,3 +181,71 @@ def test_nvls_ineligible_map_stays_p2p(monkeypatch):
         finally:
             for c in comms:
                 hc.hetccl_comm_destroy(c)
+
+
+def _nvls_rank(rank, world, port, m, q):
+    import os
+    import sys
+    ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), HETCCL_NVLS="1", HETCCL_NVLS_MB="2",
+                      HETCCL_TIMEOUT_S="20")
+    import torch
+    import torch.distributed as dist
+    import paper_2601_22585_b200 as hc
+    from harness import inputs, to_numpy, to_torch
+    torch.cuda.set_device(rank)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        comm = hc.init_process_group_comm(m)
+        on, _, _ = hc.hetccl_comm_nvls(comm)
+        why = (hc.lib().hetccl_get_last_error(comm) or b"").decode()
+        res = []
+        if on:
+            for dt, count in (("bf16", 5 * 8192 + 333), ("bf16", (3 << 20) // 2 + 5), ("f32", 65536 * 3 + 7)):
+                for it in range(2):
+                    xs = inputs("normal", 70 + it, world, count, dt)
+                    x = to_torch(xs[rank], dt, "cuda")
+                    y = torch.zeros_like(x)
+                    hc.allreduce(x, y, comm)
+                    torch.cuda.synchronize()
+                    hc.hetccl_comm_get_async_error(comm)
+                    res.append((dt, count, it, to_numpy(y, dt)))
+        hc.hetccl_comm_destroy(comm)
+        q.put((rank, bool(on), why, res))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name", ["2", "2+2"])
+def test_nvls_one_rank_per_process(name):
+    """NVLS across processes (one rank per GPU): the domain leader hands its multicast handle to the members as a
+    file descriptor over a unix socket, every member adds its device and binds its memory, and the ranks agree
+    before the comm switches to NVLS. Results: every rank bitwise identical, R7's gate (16-bit staged in fp32)."""
+    import socket
+    import torch
+    import torch.multiprocessing as mp
+    m = MAPS[name]
+    n = len(m)
+    if _ngpu() < n:
+        pytest.skip(f"needs {n} GPUs")
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_nvls_rank, args=(r, n, port, m, q)) for r in range(n)]
+    for p in ps:
+        p.start()
+    out = dict((r, (on, why, res)) for r, on, why, res in (q.get(timeout=300) for _ in range(n)))
+    for p in ps:
+        p.join(timeout=60)
+    ons = {out[r][0] for r in range(n)}
+    assert len(ons) == 1, f"ranks disagree on NVLS: {out}"
+    if not ons.pop():
+        pytest.skip(f"NVLS unavailable across processes: {out[0][1]}")
+    for j, (dt, count, it, _) in enumerate(out[0][2]):
+        xs = inputs("normal", 70 + it, n, count, dt)
+        _check([out[r][2][j][3] for r in range(n)], xs, dt, f"{name} {dt} n={count} it={it} (multi-process)", m)
