@@ -34,6 +34,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <mutex>
 
 #include "hetccl_internal.h"
 
@@ -2291,9 +2292,35 @@ static size_t dyn_smem(int op, int tma) {
   return (HETCCL_TMA && tma) ? (size_t)kTmaStages * kTmaStageBytes : 0;
 }
 
+// per-process memo of (kernel, device) -> dynamic-smem opt-in done / co-resident CTAs per SM: both are host API
+// calls that would otherwise sit on every op's launch path (small-message latency)
+struct FnMemo {
+  KernFn fn;
+  int dev;
+  size_t smem;
+  int per_sm;  // -1: not queried yet
+};
+static FnMemo g_memo[512];
+static int g_nmemo = 0;
+static std::mutex g_memo_mu;
+static FnMemo* memo(KernFn fn, size_t smem) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_memo_mu);
+  for (int i = 0; i < g_nmemo; i++)
+    if (g_memo[i].fn == fn && g_memo[i].dev == dev && g_memo[i].smem == smem) return &g_memo[i];
+  if (g_nmemo == 512) return nullptr;
+  FnMemo* m = &g_memo[g_nmemo];
+  if (smem > 0 &&  // (static + dynamic > 48 KiB needs the opt-in even for 48 KiB dynamic)
+      cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return nullptr;
+  *m = FnMemo{fn, dev, smem, -1};
+  g_nmemo++;
+  return m;
+}
 static cudaError_t allow_smem(KernFn fn, size_t bytes) {
-  if (bytes == 0) return cudaSuccess;  // (static + dynamic > 48 KiB needs the opt-in even for 48 KiB dynamic)
-  return cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (bytes == 0) return cudaSuccess;
+  return memo(fn, bytes) ? cudaSuccess : cudaErrorInvalidValue;
 }
 
 cudaError_t launch_collective(const OpArgs& a, int nlocal, int dt, int red, bool cooperative, cudaStream_t s) {
@@ -2325,9 +2352,13 @@ int max_coresident(int op, int dt, int red, int tma) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const size_t smem = dyn_smem(op, tma);
-  if (allow_smem(fn, smem) != cudaSuccess) return 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)fn, kThreads, smem) != cudaSuccess) return 0;
-  return per_sm * sms;
+  FnMemo* m = memo(fn, smem);
+  if (!m) return 0;
+  if (m->per_sm < 0) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, (const void*)fn, kThreads, smem) != cudaSuccess) return 0;
+    m->per_sm = per_sm;
+  }
+  return m->per_sm * sms;
 }
 
 }  // namespace HETCCL_KNS

@@ -179,3 +179,59 @@ def test_two_comms_two_streams_concurrently(monkeypatch):
     finally:
         for c in ca + cb:
             hc.hetccl_comm_destroy(c)
+
+
+@pytest.mark.parametrize("name", ["1+1", "2+2", "1+3", "1+1+2", "4"])
+@pytest.mark.parametrize("kernels", ["tma_s2g", "tma_st"])
+def test_collectives_on_tma_kernels(name, kernels, monkeypatch):
+    """One rank per GPU on the TMA kernel build (HETCCL_LEGACY=0; the default there is the legacy build): ring
+    movers with bulk-copy stores to NVLink peers (S2G) and with per-thread stores. All-Reduce (staged and
+    direct into symmetric buffers), Reduce-Scatter and All-Gather bitwise against the oracle."""
+    import torch
+    import paper_2601_22585_b200 as hc
+    m = MAPS[name]
+    n = len(m)
+    if _ngpu() < n:
+        pytest.skip(f"needs {n} GPUs")
+    monkeypatch.setenv("HETCCL_LEGACY", "0")
+    monkeypatch.setenv("HETCCL_S2G", "1" if kernels == "tma_s2g" else "0")
+    monkeypatch.setenv("HETCCL_NCHANNELS", "64")
+    count = (1 << 20) + 4099
+    xs = inputs("normal", 81, n, count, "bf16")
+    comms = _comms(m)
+    try:
+        ss = _streams(n)
+        sends = [to_torch(xs[r], "bf16", f"cuda:{r}") for r in range(n)]
+        recvs = [torch.zeros_like(s) for s in sends]
+        sym_x = hc.symmetric_empty_all(comms, count, torch.bfloat16)
+        sym_y = hc.symmetric_empty_all(comms, count, torch.bfloat16)
+        for r in range(n):
+            sym_x[r].copy_(sends[r])
+        _sync(n)
+        for r in range(n):
+            hc.allreduce(sends[r], recvs[r], comms[r], stream=ss[r])
+        for r in range(n):
+            hc.allreduce(sym_x[r], sym_y[r], comms[r], stream=ss[r])
+        _sync(n)
+        want = oracle.allreduce(xs, m, "bf16", "sum")
+        for r in range(n):
+            assert_matches(to_numpy(recvs[r], "bf16"), want, xs, "bf16", "sum", f"{kernels} {name} staged rank {r}")
+            assert_matches(to_numpy(sym_y[r], "bf16"), want, xs, "bf16", "sum", f"{kernels} {name} direct rank {r}")
+        R = count // n
+        rs = [torch.zeros(R, dtype=torch.bfloat16, device=f"cuda:{r}") for r in range(n)]
+        for r in range(n):
+            hc.reduce_scatter(sends[r][: n * R], rs[r], comms[r], stream=ss[r])
+        _sync(n)
+        blk = oracle.reduce_scatter([x[: n * R] for x in xs], m, "bf16", "sum")
+        ag = [torch.zeros(n * R, dtype=torch.bfloat16, device=f"cuda:{r}") for r in range(n)]
+        for r in range(n):
+            assert np.array_equal(to_numpy(rs[r], "bf16"), blk[r]), f"{kernels} {name} RS rank {r}"
+            hc.all_gather(rs[r], ag[r], comms[r], stream=ss[r])
+        _sync(n)
+        for r in range(n):
+            assert np.array_equal(to_numpy(ag[r], "bf16"), np.concatenate(blk)), f"{kernels} {name} AG rank {r}"
+        for c in comms:
+            hc.hetccl_comm_get_async_error(c)
+    finally:
+        for c in comms:
+            hc.hetccl_comm_destroy(c)
