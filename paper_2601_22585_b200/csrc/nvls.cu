@@ -44,8 +44,10 @@ namespace hetccl {
 namespace {
 
 constexpr int kNvThreads = 256;
-constexpr int kNvCounters = 4;  // N_IN, N_X, N_XACK, N_OUT
-enum : int { N_IN = 0, N_X = 1, N_XACK = 2, N_OUT = 3 };
+constexpr int kNvCounters = 5;  // N_IN, N_X, N_XACK, N_OUT, N_DONE
+enum : int { N_IN = 0, N_X = 1, N_XACK = 2, N_OUT = 3, N_DONE = 4 };
+constexpr int kNvSlots = 4;     // chunk slots of the uc buffer and of the cross slots (the pipeline is 4 deep)
+constexpr int kNvUnroll = 4;    // multicast reductions in flight per thread
 
 // ---------------------------------------------------------------- device -----------------------
 __device__ __forceinline__ uint64_t nv_ld_acquire(const uint64_t* p) {
@@ -187,6 +189,19 @@ __device__ void nv_signal(const NvlsArgs& a, int ch, int ctr, const int* who, in
 }
 
 // W: 16-bit dtype staged through an fp32 uc (a group of V elements = 16 bytes of x = UB = 32 bytes of uc)
+//
+// Software pipeline over the op's chunks (kNvSlots chunk slots in uc and in the cross slots): iteration it runs
+//   P0 copy-in of chunk it            -> signal N_IN  (domain members)
+//   P1 of chunk it-1: wait N_IN (all members) and, for slot reuse, N_XACK of chunk it-1-kNvSlots (cross
+//      receivers); multimem.ld_reduce of my segment = the domain partial -> member i of every domain's cross
+//      slot -> signal N_X
+//   P2 of chunk it-2: wait N_X, and N_DONE of chunk it-2-kNvSlots (every member copied that slot out before my
+//      multicast store overwrites it); fold the D partials, multimem.st -> signal N_XACK, N_OUT
+//   P3 of chunk it-3: wait N_OUT; copy-out -> signal N_DONE
+// Every wait is on signals peers send at an earlier iteration, so with all CTAs co-resident no cycle exists; a
+// chunk's uc slot is refilled (P0, iteration g) only after this rank's P3 of the slot's previous chunk
+// (iteration g-kNvSlots+3), which waited for every member's multicast store of it. Zero copy (send == recv == uc):
+// chunk g lives at its own place in uc, no slot is reused.
 template <int DT, bool W>
 __global__ void __launch_bounds__(kNvThreads) k_nvls_allreduce(NvlsArgs a) {
   using VV = NvVec<DT>;
@@ -230,123 +245,158 @@ __global__ void __launch_bounds__(kNvThreads) k_nvls_allreduce(NvlsArgs a) {
   __syncthreads();
   const uint64_t base = s_base;
   const size_t nchunks = (a.count + a.ce - 1) / a.ce;
-  for (size_t g = 0; g < nchunks; ++g) {
-    const uint64_t G = base + g;
-    const size_t c0 = g * a.ce;                                 // first element of the chunk
-    const size_t len = min(a.ce, a.count - c0);
-    const size_t nvec = (len + V - 1) / V;                      // vectors in the (padded) chunk
-    // every chunk of an op uses the partition of its first chunk (a short last chunk only clips it), so
-    // a uc vector always belongs to the same channel: a channel never writes the next chunk into a range
-    // another channel may still be copying out (q30); ops are ordered by the kernel boundary
-    const size_t seg = ((min(a.ce, a.count) + V - 1) / V + a.d - 1) / a.d;  // vectors per segment
-    const size_t sub = (seg + a.nch - 1) / a.nch;               // vectors per channel per segment
-    auto range = [&](int s, size_t& lo, size_t& hi) {
-      const size_t s0 = (size_t)s * seg;
-      lo = min(nvec, s0 + min(seg, (size_t)ch * sub));
-      hi = min(nvec, s0 + min(seg, (size_t)(ch + 1) * sub));
-    };
-    // ---- 1. x -> uc (every segment's channel range), zero padding past len ----
-    if (!a.zero_copy) {
-      for (int s = 0; s < a.d; s++) {
-        size_t lo, hi;
-        range(s, lo, hi);
-        for (size_t v = lo + tid; v < hi; v += nth) {
-          uint4 w;
-          if ((v + 1) * V <= len) {
-            w = nv_ld(a.send + (c0 + v * V) * ES);
-          } else {
-            w = make_uint4(0, 0, 0, 0);
-            for (int e = 0; e < V && v * V + e < len; e++) {
-              if (ES == 4) (&w.x)[e] = *(const uint32_t*)(a.send + (c0 + v * V + e) * 4);
-              else reinterpret_cast<uint16_t*>(&w)[e] = *(const uint16_t*)(a.send + (c0 + v * V + e) * 2);
+  // every chunk of an op uses the partition of its first chunk (a short last chunk only clips it), so a uc
+  // vector always belongs to the same channel (q30)
+  const size_t seg = ((min(a.ce, a.count) + V - 1) / V + a.d - 1) / a.d;  // vectors per segment
+  const size_t sub = (seg + a.nch - 1) / a.nch;                         // vectors per channel per segment
+  const size_t slot_b = (size_t)a.ce / V * UB;                           // uc bytes per chunk slot
+  auto chunk_len = [&](size_t g) { return min(a.ce, a.count - g * a.ce); };
+  auto range = [&](size_t nvec, int s, size_t& lo, size_t& hi) {
+    const size_t s0 = (size_t)s * seg;
+    lo = min(nvec, s0 + min(seg, (size_t)ch * sub));
+    hi = min(nvec, s0 + min(seg, (size_t)(ch + 1) * sub));
+  };
+  auto ucp = [&](size_t g) { return (a.zero_copy ? g : g % kNvSlots) * slot_b; };  // chunk g's offset in uc / mc
+  auto warp0_wait = [&](int ctr, const int* who, int n, int skip, uint64_t tg) {
+    if (tid < 32 && !nv_wait(a, ch, ctr, who, n, skip, tg)) s_abort = 1;
+  };
+  const long long nit = nchunks ? (long long)nchunks + 3 : 0;
+  for (long long it = 0; it < nit; ++it) {
+    // ---- P0: x -> uc (every segment's channel range), zero padding past len ----
+    if (it < (long long)nchunks) {
+      const size_t g = (size_t)it, c0 = g * a.ce, len = chunk_len(g), nvec = (len + V - 1) / V;
+      char* uc = a.uc + ucp(g);
+      if (!a.zero_copy) {
+        for (int sg = 0; sg < a.d; sg++) {
+          size_t lo, hi;
+          range(nvec, sg, lo, hi);
+          for (size_t v = lo + tid; v < hi; v += nth) {
+            uint4 w;
+            if ((v + 1) * V <= len) {
+              w = nv_ld(a.send + (c0 + v * V) * ES);
+            } else {
+              w = make_uint4(0, 0, 0, 0);
+              for (int e = 0; e < V && v * V + e < len; e++) {
+                if (ES == 4) (&w.x)[e] = *(const uint32_t*)(a.send + (c0 + v * V + e) * 4);
+                else reinterpret_cast<uint16_t*>(&w)[e] = *(const uint16_t*)(a.send + (c0 + v * V + e) * 2);
+              }
             }
-          }
-          if (W) widen_st(a.uc + v * UB, w, false);
-          else nv_st(a.uc + v * UB, w);
-        }
-      }
-      // every storing thread orders its unicast stores before the peers' reads through the multicast
-      // alias (a warp-0 fence after the barrier was not enough: q31, stale inputs in a chunk's reduce)
-      nv_fence();
-    }
-    __syncthreads();
-    if (tid < 32) {
-      nv_signal(a, ch, N_IN, a.dmem, a.d, a.i);
-      if (!nv_wait(a, ch, N_IN, a.dmem, a.d, a.i, G + 1)) s_abort = 1;
-      if (a.D > 1 && G >= 2 && !nv_wait(a, ch, N_XACK, a.xrank, a.D, a.k, G - 1)) s_abort = 1;
-      asm volatile("fence.proxy.alias;" ::: "memory");
-    }
-    __syncthreads();
-    if (s_abort) break;
-    size_t lo, hi;
-    range(a.i, lo, hi);
-    const size_t so = (size_t)(G & 1) * a.D;  // slot base (in units of xs_slot) of this chunk
-    // ---- 2. domain partial through the switch -> my cross slot + member i of every other domain ----
-    for (size_t v = lo + tid; v < hi; v += nth) {
-      uint4 p;
-      if (W) p = narrow2(mc_ld_reduce<DT_F32>(a.mc + v * UB), mc_ld_reduce<DT_F32>(a.mc + v * UB + 16));
-      else p = mc_ld_reduce<DT>(a.mc + v * UB);
-      const size_t off = (v - (size_t)a.i * seg) * 16;
-      for (int q = 0; q < a.D; q++) nv_st(a.xs[q] + (so + a.k) * a.xs_slot + off, p);
-    }
-    __syncthreads();
-    if (tid < 32) {
-      if (a.D > 1) {
-        nv_signal(a, ch, N_X, a.xrank, a.D, a.k);
-        if (!nv_wait(a, ch, N_X, a.xrank, a.D, a.k, G + 1)) s_abort = 1;
-      }
-    }
-    __syncthreads();
-    if (s_abort) break;
-    // ---- 3. fold the D partials in ascending domain id, narrow once, multicast store ----
-    char* mine = a.xs[a.k] + so * a.xs_slot;
-    for (size_t v = lo + tid; v < hi; v += nth) {
-      const size_t off = (v - (size_t)a.i * seg) * 16;
-      uint4 w = nv_ld(mine + off);
-      if (a.D > 1) {
-        float acc[V];
-#pragma unroll
-        for (int e = 0; e < V; e++) acc[e] = VV::get(w, e);
-        for (int q = 1; q < a.D; q++) {
-          const uint4 u = nv_ld(mine + (size_t)q * a.xs_slot + off);
-#pragma unroll
-          for (int e = 0; e < V; e++) acc[e] = __fadd_rn(acc[e], VV::get(u, e));
-        }
-#pragma unroll
-        for (int e = 0; e < V; e++) VV::set(w, e, acc[e]);
-      }
-      if (W) widen_st(a.mc + v * UB, w, true);
-      else mc_st(a.mc + v * UB, w);
-    }
-    __syncthreads();
-    if (tid < 32) {
-      if (a.D > 1) nv_signal(a, ch, N_XACK, a.xrank, a.D, a.k);
-      nv_signal(a, ch, N_OUT, a.dmem, a.d, a.i);
-      if (!nv_wait(a, ch, N_OUT, a.dmem, a.d, a.i, G + 1)) s_abort = 1;
-      asm volatile("fence.proxy.alias;" ::: "memory");
-    }
-    __syncthreads();
-    if (s_abort) break;
-    // ---- 4. uc -> y ----
-    if (!a.zero_copy) {
-      for (int s = 0; s < a.d; s++) {
-        size_t l2, h2;
-        range(s, l2, h2);
-        for (size_t v = l2 + tid; v < h2; v += nth) {
-          const uint4 w = W ? narrow2(nv_ld(a.uc + v * UB), nv_ld(a.uc + v * UB + 16)) : nv_ld(a.uc + v * UB);
-          if ((v + 1) * V <= len) {
-            nv_st(a.recv + (c0 + v * V) * ES, w);
-          } else {
-            for (int e = 0; e < V && v * V + e < len; e++) {
-              if (ES == 4) *(uint32_t*)(a.recv + (c0 + v * V + e) * 4) = (&w.x)[e];
-              else *(uint16_t*)(a.recv + (c0 + v * V + e) * 2) = reinterpret_cast<const uint16_t*>(&w)[e];
-            }
+            if (W) widen_st(uc + v * UB, w, false);
+            else nv_st(uc + v * UB, w);
           }
         }
+        // every storing thread orders its unicast stores before the peers' reads through the multicast alias (q31)
+        nv_fence();
       }
-      __syncthreads();  // the next chunk's copy-in overwrites uc
+      __syncthreads();
+      if (tid < 32) nv_signal(a, ch, N_IN, a.dmem, a.d, a.i);
+    }
+    // ---- P1: domain partial through the switch -> member i of every domain's cross slot ----
+    if (it >= 1 && it - 1 < (long long)nchunks) {
+      const size_t g = (size_t)(it - 1), nvec = (chunk_len(g) + V - 1) / V;
+      const uint64_t G = base + g;
+      warp0_wait(N_IN, a.dmem, a.d, a.i, G + 1);
+      if (a.D > 1 && g >= (size_t)kNvSlots) warp0_wait(N_XACK, a.xrank, a.D, a.k, G + 1 - kNvSlots);
+      __syncthreads();
+      if (s_abort) break;
+      asm volatile("fence.proxy.alias;" ::: "memory");
+      const char* mc = a.mc + ucp(g);
+      const size_t so = (g % kNvSlots) * a.D;  // cross-slot base (units of xs_slot) of this chunk
+      size_t lo, hi;
+      range(nvec, a.i, lo, hi);
+      // kNvUnroll switch reductions in flight per thread (each is a round trip through the NVSwitch)
+      for (size_t v0 = lo + tid; v0 < hi; v0 += (size_t)kNvUnroll * nth) {
+        uint4 p[kNvUnroll], p2[kNvUnroll];
+#pragma unroll
+        for (int u = 0; u < kNvUnroll; u++) {
+          const size_t v = v0 + (size_t)u * nth;
+          if (v >= hi) continue;
+          if (W) {
+            p[u] = mc_ld_reduce<DT_F32>(mc + v * UB);
+            p2[u] = mc_ld_reduce<DT_F32>(mc + v * UB + 16);
+          } else {
+            p[u] = mc_ld_reduce<DT>(mc + v * UB);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kNvUnroll; u++) {
+          const size_t v = v0 + (size_t)u * nth;
+          if (v >= hi) continue;
+          const uint4 w = W ? narrow2(p[u], p2[u]) : p[u];
+          const size_t off = (v - (size_t)a.i * seg) * 16;
+          for (int q = 0; q < a.D; q++) nv_st(a.xs[q] + (so + a.k) * a.xs_slot + off, w);
+        }
+      }
+      __syncthreads();
+      if (tid < 32 && a.D > 1) nv_signal(a, ch, N_X, a.xrank, a.D, a.k);
+    }
+    // ---- P2: fold the D partials in ascending domain id, narrow once, multicast store ----
+    if (it >= 2 && it - 2 < (long long)nchunks) {
+      const size_t g = (size_t)(it - 2), nvec = (chunk_len(g) + V - 1) / V;
+      const uint64_t G = base + g;
+      if (a.D > 1) warp0_wait(N_X, a.xrank, a.D, a.k, G + 1);
+      if (!a.zero_copy && g >= (size_t)kNvSlots) warp0_wait(N_DONE, a.dmem, a.d, -1, G + 1 - kNvSlots);
+      __syncthreads();
+      if (s_abort) break;
+      char* mc = a.mc + ucp(g);
+      const char* mine = a.xs[a.k] + (g % kNvSlots) * a.D * a.xs_slot;
+      size_t lo, hi;
+      range(nvec, a.i, lo, hi);
+      for (size_t v = lo + tid; v < hi; v += nth) {
+        const size_t off = (v - (size_t)a.i * seg) * 16;
+        uint4 w = nv_ld(mine + off);
+        if (a.D > 1) {
+          float acc[V];
+#pragma unroll
+          for (int e = 0; e < V; e++) acc[e] = VV::get(w, e);
+          for (int q = 1; q < a.D; q++) {
+            const uint4 u = nv_ld(mine + (size_t)q * a.xs_slot + off);
+#pragma unroll
+            for (int e = 0; e < V; e++) acc[e] = __fadd_rn(acc[e], VV::get(u, e));
+          }
+#pragma unroll
+          for (int e = 0; e < V; e++) VV::set(w, e, acc[e]);
+        }
+        if (W) widen_st(mc + v * UB, w, true);
+        else mc_st(mc + v * UB, w);
+      }
+      __syncthreads();
+      if (tid < 32) {
+        if (a.D > 1) nv_signal(a, ch, N_XACK, a.xrank, a.D, a.k);
+        nv_signal(a, ch, N_OUT, a.dmem, a.d, a.i);
+      }
+    }
+    // ---- P3: uc -> y ----
+    if (it >= 3) {
+      const size_t g = (size_t)(it - 3), c0 = g * a.ce, len = chunk_len(g), nvec = (len + V - 1) / V;
+      const uint64_t G = base + g;
+      warp0_wait(N_OUT, a.dmem, a.d, a.i, G + 1);
+      __syncthreads();
+      if (s_abort) break;
+      asm volatile("fence.proxy.alias;" ::: "memory");
+      if (!a.zero_copy) {
+        const char* uc = a.uc + ucp(g);
+        for (int sg = 0; sg < a.d; sg++) {
+          size_t l2, h2;
+          range(nvec, sg, l2, h2);
+          for (size_t v = l2 + tid; v < h2; v += nth) {
+            const uint4 w = W ? narrow2(nv_ld(uc + v * UB), nv_ld(uc + v * UB + 16)) : nv_ld(uc + v * UB);
+            if ((v + 1) * V <= len) {
+              nv_st(a.recv + (c0 + v * V) * ES, w);
+            } else {
+              for (int e = 0; e < V && v * V + e < len; e++) {
+                if (ES == 4) *(uint32_t*)(a.recv + (c0 + v * V + e) * 4) = (&w.x)[e];
+                else *(uint16_t*)(a.recv + (c0 + v * V + e) * 2) = reinterpret_cast<const uint16_t*>(&w)[e];
+              }
+            }
+          }
+        }
+      }
+      __syncthreads();  // this slot's copy-out is done: members may multicast-store the slot's next chunk
+      if (tid < 32) nv_signal(a, ch, N_DONE, a.dmem, a.d, -1);
     }
   }
+  __syncthreads();
   if (tid == 0 && !s_abort) *nv_base(a, ch) = base + nchunks;
 }
 
@@ -911,7 +961,13 @@ cudaError_t nvls_allreduce(NvlsState* s, const void* send, void* recv, size_t co
   a.send = (const char*)send;
   a.recv = (char*)recv;
   a.count = count;
-  a.ce = s->ce_bytes / (wide ? 4 : es);  // elements per chunk: uc holds fp32 when staging wide
+  // kNvSlots chunk slots in uc (uc holds fp32 when staging wide); slot bytes a multiple of 16 * d so every
+  // segment starts on a vector
+  const size_t unit = (size_t)16 * a.d;
+  const size_t chunk_b = std::max(unit, s->ce_bytes / kNvSlots / unit * unit);
+  a.ce = chunk_b / (wide ? 4 : es);  // elements per chunk
+  const size_t V = (dt == DT_F32) ? 4 : 8;
+  a.xs_slot = ((a.ce / V + a.d - 1) / a.d) * 16;  // one domain partial of one member's segment of a chunk
   a.err = err;
   a.timeout_ns = timeout_ns;
   a.wide = wide;

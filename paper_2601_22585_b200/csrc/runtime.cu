@@ -501,7 +501,7 @@ hetcclResult_t hetccl_comm_init(hetcclComm_t* comm, int nranks, int rank, const 
   // connect hands it to the members (hetccl_comm_nvls reports whether the comm ended up in NVLS mode)
   if (nranks > 1 && env_long("HETCCL_NVLS", 0) == 1) {
     char why[256] = {0};
-    const size_t mb = (size_t)std::max(1L, env_long("HETCCL_NVLS_MB", 32));
+    const size_t mb = (size_t)std::max(1L, env_long("HETCCL_NVLS_MB", 128));
     const int nch = (int)std::max(1L, std::min(1024L, env_long("HETCCL_NVLS_NCH", 148)));
     if (nvls_proc_begin(c->topo, rank, cuda_device, mb << 20, nch, &c->nvls_pending, &c->nvls_blob, why, sizeof(why)))
       c->last_error = why;
@@ -641,7 +641,7 @@ hetcclResult_t hetccl_comm_init_all(hetcclComm_t* comms, int ndev, const int* de
     if (env_long("HETCCL_NVLS", 0) == 1) {
       NvlsState* st[kMaxRanks] = {nullptr};
       char why[256] = {0};
-      const size_t mb = (size_t)std::max(1L, env_long("HETCCL_NVLS_MB", 32));
+      const size_t mb = (size_t)std::max(1L, env_long("HETCCL_NVLS_MB", 128));
       const int nch = (int)std::max(1L, std::min(1024L, env_long("HETCCL_NVLS_NCH", 148)));
       if (nvls_create(ndev, devlist, t, mb << 20, nch, st, why, sizeof(why)) == 0) {
         for (int i = 0; i < ndev; i++) cs[i]->nvls = st[i];
