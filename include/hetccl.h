@@ -116,7 +116,9 @@ HETCCL_API hetcclResult_t hetccl_comm_info(hetcclComm_t comm, int* rank, int* nr
 
 /*
  * NVLS mode (opt-in). With HETCCL_NVLS=1 in the environment of
- * hetccl_comm_init_all, and every domain of the same size d >= 2 on devices with multicast support,
+ * hetccl_comm_init_all or of every rank's hetccl_comm_init (one rank per process: the domain leader hands its
+ * multicast handle to the members through a unix socket during hetccl_comm_connect, and the ranks agree before
+ * switching), and every domain of the same size d >= 2 on devices with multicast support,
  * each domain gets an NVLink SHARP multicast object and hetccl_allreduce (bf16/fp16/fp32 sum, 16-byte
  * aligned buffers) runs its intra-domain reduce-scatter inside the switch (multimem.ld_reduce) and its
  * intra-domain all-gather as one multicast store (multimem.st); the cross-domain exchange and fold stay
