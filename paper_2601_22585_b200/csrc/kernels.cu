@@ -1,12 +1,15 @@
 // kernels.cu — sm_100a device code of the hierarchical collectives.
 //
-// One persistent CTA per (channel, local rank), 128 threads, two CTAs per SM. Every op is a short list
+// One persistent CTA per (channel, local rank), 128 threads; compiled twice (hetccl_internal.h): the TMA build
+// (namespace k4, 4 CTAs per SM, sources staged by TMA bulk copies into a shared-memory ring and results stored by
+// bulk copies, "tma_move") and the legacy build (k2, kernels_legacy.cu, 2 CTAs per SM, sources staged by
+// cp.async, 16-byte register stores). Every op is a short list
 // of stages (All-Reduce: A intra push, B domain fold of the other domains' pieces + cross push, C
 // domain fold of my pieces + cross fold + all-gather writes, D intra forward, E completion); a channel
 // runs them as a SOFTWARE PIPELINE over its tiles t = ch, ch+nch, ...: iteration i runs the stage at
 // position p on the channel's tile i-p, so the intra- and cross-domain stages of different tiles overlap
-// and no flag round trip sits on the critical path (run_pipeline). Data moves with 16-byte vector
-// loads/stores (plus an L2 bulk prefetch of the next batches); stores go straight into a peer's
+// and no flag round trip sits on the critical path (run_pipeline). Data moves through the movers below;
+// stores go straight into a peer's
 // IPC-mapped scratch slot, or — when every rank's recv buffer is addressable (rank-multiplexed comms,
 // symmetric buffers) — straight into the peers' recv buffers ("direct"), and the domain fold may read
 // the peers' send buffers ("pull", rank-multiplexed comms). Hand-off between stages uses per-(receiver,
@@ -567,9 +570,11 @@ __device__ __noinline__ void tma_stream_dyn(int ni, int D, int kpos, int nd, uin
     }
     return cur++;
   };
+  const int s2g = g_s2g;
   auto issue = [&](uint32_t k) {
     const unsigned g = seq0 + k, st = g % kTmaStages, u = g / kTmaStages;
     if (u > 0) mbar_wait(&g_empty[st], (u - 1) & 1u);
+    if (s2g && u > 0) bulk_wait_read();
     const long long c = next_chunk();
     *(volatile int*)&g_chunk_of[st] = (int)c;
     if (c < 0) {
@@ -600,7 +605,7 @@ __device__ __noinline__ void tma_stream_dyn(int ni, int D, int kpos, int nd, uin
       if (lane == 0) mbar_arrive(&g_empty[st]);
       break;
     }
-    const unsigned char* sb = g_ring + st * kTmaStageBytes;
+    unsigned char* sb = g_ring + st * kTmaStageBytes;
     const uint32_t lim = min(cv, nv - (uint32_t)c * cv);
     for (uint32_t idx = tid; idx < lim; idx += nth) {
       uint4 o = *(const uint4*)(sb + idx * 16);
@@ -632,16 +637,30 @@ __device__ __noinline__ void tma_stream_dyn(int ni, int D, int kpos, int nd, uin
         for (int e = 0; e < V; e++) Vec<S>::set(o, e, TR::narrow(acc[e]));
       }
       const size_t off = ((size_t)c * cv + idx) * 16;
-      if (hint) {
+      if (s2g) {
+        *(uint4*)(sb + idx * 16) = o;  // operand 0's slot: only this thread read it
+      } else if (hint) {
         for (int d = 0; d < nd; d++) st_v4_hint(g_dst[d] + off, o, pol_first);
       } else {
         for (int d = 0; d < nd; d++) st_v4(g_dst[d] + off, o);
+      }
+    }
+    if (s2g) {  // as in tma_stream: one bulk store per destination
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      data_bar();
+      if (tid == 0) {
+        for (int d = 0; d < nd; d++) {
+          if (hint) bulk_s2g_hint(g_dst[d] + (size_t)c * chb, sb, lim * 16, pol_first);
+          else bulk_s2g(g_dst[d] + (size_t)c * chb, sb, lim * 16);
+        }
+        bulk_commit();
       }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&g_empty[st]);
     mine++;
   }
+  if (s2g && tid == 0) bulk_wait_all();
   *(volatile unsigned*)&g_seq = seq0 + k;  // every data thread writes the same values
   *(volatile unsigned*)&g_claimed = mine;
 }
