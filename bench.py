@@ -506,6 +506,9 @@ def run_dist(args):
 
 # ---------------------------------------------------------------------------------- reference arm
 def run_reference(args):
+    """The tier's reference arm: the CPU oracle as it stands, on the box's host cores (elements split across
+    threads by oracle.allreduce_threaded, bit-identical to the serial oracle; the single-thread time is reported
+    beside it), each step a bounded sample of the same workload. Rank 0 only under torchrun."""
     rank = int(os.environ.get("RANK", 0))
     if rank != 0:
         return
@@ -515,27 +518,36 @@ def run_reference(args):
     m = MAPS.get(n_gpu, MAPS[1])
     n = len(m)
     count = args.mib * (1 << 20) // 2
+    cores = os.cpu_count() or 1
     budget = 150.0  # seconds for warmup + steps together
     per_step = budget / max(1, args.steps + args.warmup)
-    sample = int(min(count, max(1 << 14, per_step / (5e-9 * n))))
+    sample = int(min(count, max(1 << 14, per_step / (5e-9 * n / min(cores, 8)))))
     xs = gen_inputs(n, sample)
     for _ in range(args.warmup):
-        oracle.allreduce(xs, m, "bf16", "sum")
+        oracle.allreduce_threaded(xs, m, "bf16", "sum", threads=cores)
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        oracle.allreduce(xs, m, "bf16", "sum")
+        oracle.allreduce_threaded(xs, m, "bf16", "sum", threads=cores)
         times.append(time.perf_counter() - t0)
     t = sum(times) / len(times)
+    ns = min(sample, 1 << 22)
+    t0 = time.perf_counter()
+    oracle.allreduce([x[:ns] for x in xs], m, "bf16", "sum")
+    t1 = time.perf_counter() - t0
     _, bus = busbw(sample * 2, t, n)
-    desc = f"first {sample} of {count} elements per rank, {n} ranks ({SPLIT_NAME.get(n_gpu, '')}), single-threaded"
+    _, bus1 = busbw(ns * 2, t1, n)
+    workload = (f"C2 target point: hierarchical All-Reduce, {args.mib} MiB bf16 per rank, {SPLIT_NAME[1]}" if n_gpu == 1
+                else f"hierarchical All-Reduce, {args.mib} MiB bf16 per rank, {SPLIT_NAME.get(n_gpu, '')}")
+    desc = (f"first {sample} of {count} elements per rank, {n} ranks ({SPLIT_NAME.get(n_gpu, '')}), {cores} host threads "
+            f"(elements split across threads); single thread on the first {ns}: {bus1:.4f} GB/s")
     out = {
         "impl": "reference", "metric": "allreduce_busbw", "value": round(bus, 4), "unit": "GB/s", "n_gpus": n_gpu,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded bf16 N(0,1)*2^-4)",
-        "config": {"workload": f"hierarchical All-Reduce, {args.mib} MiB bf16 per rank, {SPLIT_NAME.get(n_gpu, '')}",
-                   "ranks": n, "rank_to_domain": m, "count": count},
-        "cpu_baseline": {"value": round(bus, 4), "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": desc},
+        "config": {"workload": workload, "ranks": n, "rank_to_domain": m, "count": count},
+        "cpu_baseline": {"value": round(bus, 4), "unit": "GB/s", "cores": cores, "kind": "oracle", "sample": desc,
+                         "single_thread": {"value": round(bus1, 4), "unit": "GB/s", "cores": 1}},
         "e2e": {"value": round(bus, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
