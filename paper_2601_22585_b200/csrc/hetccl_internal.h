@@ -129,7 +129,8 @@ struct OpArgs {
   int tma;                      // 1: the movers stage their sources through the TMA ring (dynamic shared memory)
   int l2hint;                   // 1: L2 policies in the TMA movers (evict_first streams, evict_last + discard partials)
   int spacing;                  // plain pipeline (ws == 0): positions between consecutive stages (1 = adjacent)
-  int steal;                    // 1: All-Reduce C stages are published as units other channels of the rank may take
+  int steal;                    // > 0: that percentage of each All-Reduce C stage is published for the rank's other
+                                //   channels to take (100: all of it), 0 off
   int s2g;                      // 1: the TMA movers store results with bulk copies shared -> global
 };
 

@@ -1294,7 +1294,14 @@ struct Pipe {
         g_claimed = 0;
       }
       data_bar();
-      op.stage(2, t, slot);  // its ring mover publishes the job and claims from the front
+      if (a.steal < 100) {  // the static part first, at full speed (bulk-copy stores, no claims)
+        if (tid == 0) g_claim_mode = 0;
+        data_bar();
+        op.stage_c_part(t, slot, 0, a.steal);
+        if (tid == 0) g_claim_mode = 1;
+        data_bar();
+      }
+      op.stage_c_part(t, slot, 1, a.steal);  // its ring mover publishes the tail job and claims from the front
       data_bar();
       if (tid == 0) {
         g_claim_mode = 0;
@@ -1335,7 +1342,7 @@ struct Pipe {
           const uint64_t tag = g_claim_tag;
           Op vop(a, blockIdx.y, v);
           const size_t tv = (size_t)v + (size_t)(tag >> 52) * a.nch;
-          vop.stage(2, tv, (int)((tag >> 48) & 15u));  // vector part of the victim's C through my ring
+          vop.stage_c_part(tv, (int)((tag >> 48) & 15u), 1, a.steal);  // vector part of the victim's tail
           data_bar();
           if (tid == 0) {
             g_claim_mode = 0;
@@ -1608,6 +1615,22 @@ struct ArOp {
     int np = 0;
     for (int sg = s_lo; sg < s_hi; sg++) np += g.piece(sg, k + 1) > g.piece(sg, k);
     return np;
+  }
+  // stage C of tile t (single piece) split at a 64-element boundary: part 0 = the first (100 - tail_pct)% run
+  // statically by the owner, part 1 = the tail it publishes for chunk stealing (tail_pct = 100: all of it)
+  __device__ void stage_c_part(size_t t, int slot, int part, int tail_pct) {
+    const size_t tb = t * TL, len = min(TL, a.count - tb);
+    const Geo g{len, TL, L, D};
+    const size_t r0 = g.seg(s_lo);
+    T* my_s2 = slot_ptr<T>(a, me, ch, slot) + s2_off(d);
+    for (int sg = s_lo; sg < s_hi; sg++) {
+      const size_t c0 = g.piece(sg, k), c1 = g.piece(sg, k + 1);
+      if (c1 <= c0) continue;
+      const size_t tail = min(c1 - c0, ((c1 - c0) * (size_t)tail_pct / 100 + 63) / 64 * 64);
+      const size_t cm = c1 - tail;
+      if (part == 0 && cm > c0) fold_c(g, sg, tb, c0, cm, slot, r0, my_s2);
+      if (part == 1 && c1 > cm) fold_c(g, sg, tb, cm, c1, slot, r0, my_s2);
+    }
   }
   static constexpr bool kSteal = true;  // stage 2 can be split into units other channels may take
   __device__ void stage(int s, size_t t, int slot) {

@@ -35,8 +35,8 @@ PROTOS = {
                             "HETCCL_NSLOTS": "12"},
     "gpu_pull_ws2": {"HETCCL_SYS_SCOPE": "0", "HETCCL_WS": "2", "HETCCL_NSLOTS": "12"},
     # C-stage chunk stealing (opt-in): one tile per channel so jobs are published and taken by other channels
-    "gpu_pull_steal": {"HETCCL_SYS_SCOPE": "0", "HETCCL_STEAL": "1", "HETCCL_TILE_KB": "4096"},
-    "sys_push_direct_steal": {"HETCCL_SYS_SCOPE": "1", "HETCCL_PULL": "0", "HETCCL_DIRECT": "1", "HETCCL_STEAL": "1",
+    "gpu_pull_steal": {"HETCCL_SYS_SCOPE": "0", "HETCCL_STEAL": "100", "HETCCL_TILE_KB": "4096"},
+    "sys_push_direct_steal": {"HETCCL_SYS_SCOPE": "1", "HETCCL_PULL": "0", "HETCCL_DIRECT": "1", "HETCCL_STEAL": "25",
                               "HETCCL_TILE_KB": "4096"},
 }
 SPLITS = ["1+1", "2+2", "4+4", "2+6", "2+2+4", "1+2+3"]
