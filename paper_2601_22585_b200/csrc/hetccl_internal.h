@@ -131,6 +131,7 @@ struct OpArgs {
   int spacing;                  // plain pipeline (ws == 0): positions between consecutive stages (1 = adjacent)
   int steal;                    // > 0: that percentage of each All-Reduce C stage is published for the rank's other
                                 //   channels to take (100: all of it), 0 off
+  int steal_help;               // 1: channels that finished their pipeline take published chunks (else owners only)
   int s2g;                      // 1: the TMA movers store results with bulk copies shared -> global
 };
 

@@ -1320,40 +1320,51 @@ struct Pipe {
       return true;
     }
   }
-  // after my own pipeline: take chunks of the rank's other channels' published C stages
+  // after my own pipeline: take chunks of the rank's other channels' published C stages. Thread 0 scans every
+  // job word without a barrier and the data threads sync once per job found, so a CTA with nothing to take
+  // leaves at once (a barrier per victim kept idle helpers around long enough to delay the kernel, r02bp).
   __device__ void help_others() {
     if constexpr (Op::kSteal) {
       const int tid = (int)threadIdx.x - g_dbase;
-      for (int kk = 1; kk < a.nch; kk++) {
-        const int v = (ch + kk) % a.nch;
-        uint64_t* sw = chan_flags(a, me, v) + (size_t)kCounters * kLineWords;
-        for (;;) {
-          if (tid == 0) {
+      __shared__ int s_victim;
+      int start = 1;
+      for (;;) {
+        if (tid == 0) {
+          s_victim = -1;
+          for (int kk = start; kk < a.nch; kk++) {
+            const int v = (ch + kk) % a.nch;
+            uint64_t* sw = chan_flags(a, me, v) + (size_t)kCounters * kLineWords;
             const uint64_t w = ld_acquire_gpu(sw);
-            const bool open = (w & 0xffffffull) < ((w >> 24) & 0xffffffull);
-            g_claim = sw;
-            g_claim_mode = open ? 2 : 0;
-            g_claim_tag = w & kTagMask;
-            g_claimed = 0;
-            g_vec_only = 1;
-          }
-          data_bar();
-          if (!g_claim_mode) break;
-          const uint64_t tag = g_claim_tag;
-          Op vop(a, blockIdx.y, v);
-          const size_t tv = (size_t)v + (size_t)(tag >> 52) * a.nch;
-          vop.stage_c_part(tv, (int)((tag >> 48) & 15u), 1, a.steal);  // vector part of the victim's tail
-          data_bar();
-          if (tid == 0) {
-            g_claim_mode = 0;
-            g_vec_only = 0;
-            if (g_claimed) {
-              fence_acq_rel(a.gpu_scope);  // my stores (peers' y included) before the owner's acquire
-              red_add_relaxed(sw + 1, g_claimed, 1);
+            if ((w & 0xffffffull) < ((w >> 24) & 0xffffffull)) {
+              s_victim = kk;
+              g_claim = sw;
+              g_claim_mode = 2;
+              g_claim_tag = w & kTagMask;
+              g_claimed = 0;
+              g_vec_only = 1;
+              break;
             }
           }
-          data_bar();
         }
+        data_bar();
+        const int kk = s_victim;
+        if (kk < 0) break;
+        start = kk;  // the same victim may still have chunks; the scan moves on once it is exhausted
+        const int v = (ch + kk) % a.nch;
+        const uint64_t tag = g_claim_tag;
+        Op vop(a, blockIdx.y, v);
+        const size_t tv = (size_t)v + (size_t)(tag >> 52) * a.nch;
+        vop.stage_c_part(tv, (int)((tag >> 48) & 15u), 1, a.steal);  // vector part of the victim's tail
+        data_bar();
+        if (tid == 0) {
+          g_claim_mode = 0;
+          g_vec_only = 0;
+          if (g_claimed) {
+            fence_acq_rel(a.gpu_scope);  // my stores (peers' y included) before the owner's acquire
+            red_add_relaxed(g_claim + 1, g_claimed, 1);
+          }
+        }
+        data_bar();
       }
       if (tid == 0) {
         g_claim_mode = 0;
@@ -1492,7 +1503,7 @@ __device__ __forceinline__ void run_pipeline(const OpArgs& a, Op& op, int me, in
     }
   }
   // ---- help the rank's other channels with their published C stages (HETCCL_STEAL) ----
-  if (a.steal && !*(volatile int*)&ps.abort_ && !(ws && sync_warp)) P.help_others();
+  if (a.steal && a.steal_help && !*(volatile int*)&ps.abort_ && !(ws && sync_warp)) P.help_others();
   __syncthreads();
   // ---- final stage (direct All-Reduce's E): one wait for every tile's signal instead of a position ----
   if (a.final_stage >= 0 && ((a.active >> a.final_stage) & 1u) && threadIdx.x < 32 && P.lane < P.n &&

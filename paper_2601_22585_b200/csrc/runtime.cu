@@ -338,6 +338,7 @@ hetcclResult_t run_op(hetcclComm_t c, int op, const void* const* sends, void* co
   // but the claims cost more than the tail they remove: r02an/r02ao mux 503-505 -> 473-476 GB/s)
   // HETCCL_STEAL = the percentage of each C stage published for stealing (100: all of it), 0 off
   a.steal = op == OP_ALLREDUCE ? (int)std::max(0L, std::min(100L, env_long("HETCCL_STEAL", 0))) : 0;
+  a.steal_help = (int)env_long("HETCCL_STEAL_HELP", 1);
   // results leave the TMA movers as bulk copies shared -> global (r02at: mux 501 -> 517 GB/s; across GPUs on the
   // TMA kernels 2+2 at 148 channels 513 -> 530, 1+1 376 -> 446)
   a.s2g = (int)env_long("HETCCL_S2G", 1);
