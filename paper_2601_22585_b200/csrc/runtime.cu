@@ -59,6 +59,8 @@ struct hetcclComm {
   size_t os_bytes = 0;                    // HETCCL_ONESHOT_KB: one-shot AR up to this many bytes per rank
   size_t os_chan = 0;                     // bytes per (buffer, sender, channel): each channel owns its region
   size_t os_stride = 0;                   // bytes per (buffer, sender) of the one-shot area = nch_max * os_chan
+  int mid_nch = 128;                      // HETCCL_MID_NCH: channel cap of one-shot and mid-size All-Reduce
+  size_t mid_bytes = 0;                   // HETCCL_MID_MB: pipelined All-Reduce up to this size takes the cap
   unsigned long long* trace = nullptr;
   size_t trace_bytes = 0;
   int trace_shape[2] = {0, 0};            // local ranks, channels of the last traced op
@@ -90,6 +92,8 @@ struct Blob {
   int ws;
   int nslots;
   unsigned long long os_bytes;
+  int mid_nch;
+  unsigned long long mid_bytes;
   cudaIpcMemHandle_t handle;
   NvlsBlob nvls;
 };
@@ -123,9 +127,11 @@ long env_long(const char* name, long dflt) {
 // One-shot regions are private per channel: channel ch's double buffer (parity of ITS op counter) and its
 // ACK only order that channel's own reuse, so a region must never be shared between channels of different
 // ops (the channel count follows the message size).
+constexpr size_t kOsChanMin = 32768;
 void set_os_layout(hetcclComm* c) {
   const size_t per = (c->os_bytes + (size_t)c->nch_max - 1) / (size_t)c->nch_max;
-  c->os_chan = c->os_bytes ? (std::max<size_t>(per, 8192) + 256 + 255) / 256 * 256 : 0;
+  // at least kOsChanMin per channel so mid one-shot sizes can run on fewer, fuller channels (run_op)
+  c->os_chan = c->os_bytes ? (std::max<size_t>(per, kOsChanMin) + 256 + 255) / 256 * 256 : 0;
   c->os_stride = (size_t)c->nch_max * c->os_chan;
 }
 size_t scratch_slots_bytes(const hetcclComm* c) { return (size_t)c->nch_max * c->nslots * c->slot_bytes; }
@@ -159,6 +165,13 @@ void read_env(hetcclComm* c) {
   const long os_default_kb = c->topo.n > 1 ? 16384L / (c->topo.n - 1) : 0;
   c->os_bytes = (size_t)std::max(0L, env_long("HETCCL_ONESHOT_KB", os_default_kb)) * 1024;
   set_os_layout(c);
+  // mid sizes (r02bv/r02bw, 2+2): one tile per channel either way, and 128 channels of larger tiles beat 296 of
+  // small ones from 2 to 32 MiB (0.89-1.03x NCCL vs 0.74-0.91x); 1+1 keeps every channel for its pipelined sizes
+  // (> 16 MiB: 0.85-0.99x at 128 vs 0.87-1.06x), so the pipelined cap applies only where a domain has >= 2 ranks
+  c->mid_nch = (int)std::max(1L, std::min((long)kMaxChannels, env_long("HETCCL_MID_NCH", 128)));
+  int dmax = 1;
+  for (int k = 0; k < c->topo.D; k++) dmax = std::max(dmax, c->topo.dom_size[k]);
+  c->mid_bytes = (size_t)std::max(0L, env_long("HETCCL_MID_MB", dmax >= 2 ? 32 : 0)) << 20;
   c->alloc_bytes = alloc_bytes_for(c);
 }
 
@@ -298,8 +311,14 @@ hetcclResult_t run_op(hetcclComm_t c, int op, const void* const* sends, void* co
     if (cap < nlocal) return fail(c, hetcclInternalError, "device cannot co-schedule %d ranks", nlocal);
     nch_max = std::min(nch_max, cap / nlocal);
   }
-  if (oneshot) {  // NEXT-3: one round trip; ~8 KiB of every rank's buffer per channel
-    a.nch = (int)std::max<size_t>(1, std::min<size_t>((size_t)nch_max, (count * (size_t)es + 8191) / 8192));
+  const size_t bytes = count * (size_t)es;
+  if (oneshot) {  // NEXT-3: one round trip; ~8 KiB of every rank's buffer per channel up to mid_nch channels, then
+    // up to kOsChanMin per channel, then every channel (r02bw: 128 channels 1.03-1.74x NCCL at 2-4 MiB vs
+    // 0.86-1.57x on 256-296; from 8 MiB the chunk grows past 32 KiB and more channels win again)
+    const size_t want = std::max<size_t>(std::min<size_t>((bytes + 8191) / 8192, (size_t)c->mid_nch),
+                                         (bytes + kOsChanMin - 1) / kOsChanMin);
+    const size_t fit = c->os_chan ? (bytes + c->os_chan - 257) / (c->os_chan - 256) : 1;
+    a.nch = (int)std::max<size_t>(1, std::min<size_t>((size_t)nch_max, std::max(want, fit)));
     // the kernel's per-channel chunk (a multiple of the vector width) must fit the channel's private region
     const size_t V = 16 / (size_t)es;
     const size_t chunk = (count + (size_t)a.nch * V - 1) / ((size_t)a.nch * V) * V;
@@ -316,6 +335,7 @@ hetcclResult_t run_op(hetcclComm_t c, int op, const void* const* sends, void* co
     CUDA_TRY(c, k4::launch_collective(a, nlocal, dt, red, c->kind == KIND_MUX, stream));
     return hetcclSuccess;
   }
+  if (c->kind != KIND_MUX && op == OP_ALLREDUCE && bytes <= c->mid_bytes) nch_max = std::min(nch_max, c->mid_nch);
   const size_t slot_elems = c->slot_bytes / (size_t)es;
   Geometry geo = make_geometry(c->topo, op, count, es, nch_max, slot_elems, c->tile_base);
   if (slot_mult_num(c->topo, op, geo.tile) > slot_elems)
@@ -528,6 +548,8 @@ hetcclResult_t hetccl_comm_export(hetcclComm_t c, void* blob, size_t* blob_bytes
   b.ws = c->ws;
   b.nslots = c->nslots;
   b.os_bytes = c->os_bytes;
+  b.mid_nch = c->mid_nch;
+  b.mid_bytes = c->mid_bytes;
   b.nvls = c->nvls_blob;
   DevGuard g(c->device);
   CUDA_TRY(c, cudaIpcGetMemHandle(&b.handle, c->local[0]));
@@ -552,8 +574,8 @@ hetcclResult_t hetccl_comm_connect(hetcclComm_t c, const void* blobs, size_t blo
     if (memcmp(b.map, c->map, sizeof(int) * c->n) != 0)
       return fail(c, hetcclInvalidUsage, "rank %d passed a different rank_to_domain map", r);
     if (b.slot_bytes != c->slot_bytes || b.nch_max != c->nch_max || b.ws != c->ws || b.nslots != c->nslots ||
-        b.os_bytes != c->os_bytes)
-      return fail(c, hetcclInvalidUsage, "rank %d has different HETCCL_SLOT_KB/NCHANNELS/WS/NSLOTS", r);
+        b.os_bytes != c->os_bytes || b.mid_nch != c->mid_nch || b.mid_bytes != c->mid_bytes)
+      return fail(c, hetcclInvalidUsage, "rank %d has different HETCCL_SLOT_KB/NCHANNELS/WS/NSLOTS/ONESHOT_KB/MID_*", r);
     if (r == c->rank) continue;
     void* p = nullptr;
     cudaError_t e = cudaIpcOpenMemHandle(&p, b.handle, cudaIpcMemLazyEnablePeerAccess);
