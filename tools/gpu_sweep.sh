@@ -4,7 +4,7 @@
 O=gpurun_out/${TAG:-sweep}; mkdir -p $O
 for e in ${ENVS:-NONE=1}; do
   env ${e//,/ } timeout 400 python -m torch.distributed.run --nnodes=1 --nproc-per-node ${N:-4} --master-addr 127.0.0.1 \
-    --master-port 29$((RANDOM%800+100)) tools/report.py --what ar_sweep --mibs ${MIBS:-2,4,8,16,32,64,128} \
+    --master-port 29$((RANDOM%800+100)) tools/report.py --what ar_sweep --mibs ${MIBS:-2,4,8,16,32,64,128} ${RARGS} \
     --out $O/s_$e.jsonl > $O/s_$e.txt 2>&1
   echo "$e" >> $O/sweep.txt
   python - "$O/s_$e.jsonl" >> $O/sweep.txt <<'EOF'

@@ -37,6 +37,7 @@ def main():
     ap.add_argument("--what", default="ar_sweep")
     ap.add_argument("--out", default=None)
     ap.add_argument("--iters", type=int, default=10)
+    ap.add_argument("--split", default=None, help="ar_sweep split (default: 1+1 / 2+2 / 4+4 by world size)")
     ap.add_argument("--mibs", default="1,2,4,8,16,32,64,128,256,512,1024", help="ar_sweep sizes (MiB per rank)")
     ap.add_argument("--kibs", default=None, help="ar_sweep sizes in KiB per rank (overrides --mibs; 1 KiB - 1 MiB "
                                                  "is the latency regime, NEXT-3)")
@@ -165,7 +166,7 @@ def main():
         del x, y, z
 
     if args.what == "ar_sweep":
-        name = DEFAULT[world]
+        name = args.split or DEFAULT[world]
         m = SPLITS[world][name]
         if args.kibs:
             for kib in [int(v) for v in args.kibs.split(",")]:
