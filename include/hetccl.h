@@ -201,7 +201,9 @@ HETCCL_API hetcclResult_t hetccl_mux_all_to_all(const void* const* sendbufs, voi
  * 4 reduce, 5 all_to_all (count = elements per block).
  * count = the op's `count` argument (recvcount / sendcount for RS / AG). Writes bytes sent and
  * received by `rank` over the peer fabric, and the tile geometry (elements per tile, tiles,
- * channels) the launch would use with `nchannels` channels (0 = default).
+ * channels) the pipelined launch would use with `nchannels` channels (0 = a one-rank-per-GPU comm's
+ * default under the current environment, including the mid-size All-Reduce channel cap; sizes that
+ * take the one-shot All-Reduce below its cutoff are reported as if pipelined).
  */
 typedef struct {
   size_t bytes_sent;

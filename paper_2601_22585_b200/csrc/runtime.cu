@@ -887,7 +887,8 @@ hetcclResult_t hetccl_plan_info(int nranks, const int* rank_to_domain, int rank,
   tmp.topo = t;
   read_env(&tmp);
   const int es = dtype_size(dt);
-  const int nch = nchannels > 0 ? std::min(nchannels, kMaxChannels) : tmp.nch_max;
+  int nch = nchannels > 0 ? std::min(nchannels, kMaxChannels) : tmp.nch_max;
+  if (nchannels <= 0 && op == OP_ALLREDUCE && count * (size_t)es <= tmp.mid_bytes) nch = std::min(nch, tmp.mid_nch);
   Geometry g = make_geometry(t, op, count, es, nch, tmp.slot_bytes / es, tmp.tile_base);
   memset(info, 0, sizeof(*info));
   plan_bytes(t, op, rank, root, count, es, g.tile, &info->bytes_sent, &info->bytes_recv);
