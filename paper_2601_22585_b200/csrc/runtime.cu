@@ -57,6 +57,7 @@ struct hetcclComm {
   int legacy = 0;                         // HETCCL_LEGACY: pipeline ops on the legacy kernels (k2), else k4
   int nslots = 8;                         // HETCCL_NSLOTS: scratch ring depth
   size_t os_bytes = 0;                    // HETCCL_ONESHOT_KB: one-shot AR up to this many bytes per rank
+  size_t os_plain_bytes = 0;              // HETCCL_ONESHOT_PLAIN_KB: the cutoff when recv is not a symmetric buffer
   size_t os_chan = 0;                     // bytes per (buffer, sender, channel): each channel owns its region
   size_t os_stride = 0;                   // bytes per (buffer, sender) of the one-shot area = nch_max * os_chan
   int mid_nch = 128;                      // HETCCL_MID_NCH: channel cap of one-shot and mid-size All-Reduce
@@ -92,6 +93,7 @@ struct Blob {
   int ws;
   int nslots;
   unsigned long long os_bytes;
+  unsigned long long os_plain_bytes;
   int mid_nch;
   unsigned long long mid_bytes;
   cudaIpcMemHandle_t handle;
@@ -129,9 +131,10 @@ long env_long(const char* name, long dflt) {
 // ops (the channel count follows the message size).
 constexpr size_t kOsChanMin = 32768;
 void set_os_layout(hetcclComm* c) {
-  const size_t per = (c->os_bytes + (size_t)c->nch_max - 1) / (size_t)c->nch_max;
+  const size_t cut = std::max(c->os_bytes, c->os_plain_bytes);
+  const size_t per = (cut + (size_t)c->nch_max - 1) / (size_t)c->nch_max;
   // at least kOsChanMin per channel so mid one-shot sizes can run on fewer, fuller channels (run_op)
-  c->os_chan = c->os_bytes ? (std::max<size_t>(per, kOsChanMin) + 256 + 255) / 256 * 256 : 0;
+  c->os_chan = cut ? (std::max<size_t>(per, kOsChanMin) + 256 + 255) / 256 * 256 : 0;
   c->os_stride = (size_t)c->nch_max * c->os_chan;
 }
 size_t scratch_slots_bytes(const hetcclComm* c) { return (size_t)c->nch_max * c->nslots * c->slot_bytes; }
@@ -167,6 +170,11 @@ void read_env(hetcclComm* c) {
   // (measured with CUDA graphs: 1+1 one-shot beats the pipeline up to 16 MiB; 2+2 up to ~4 MiB)
   const long os_default_kb = c->topo.n > 1 ? 16384L / (c->topo.n - 1) : 0;
   c->os_bytes = (size_t)std::max(0L, env_long("HETCCL_ONESHOT_KB", os_default_kb)) * 1024;
+  // plain (non-symmetric) recv buffers: the pipelined path stages results through scratch, so the one-shot
+  // wins up to twice the cutoff (r02ch / r02ci: 1+1 at 24 / 32 MiB 302 / 326 vs 244 / 277 GB/s, 2+2 at 6 MiB
+  // 149 vs 124; symmetric buffers lose there). Rank-multiplexed comms always write results directly.
+  const long os_plain_default_kb = (long)(c->os_bytes >> 10) * (c->kind == KIND_MUX ? 1 : 2);
+  c->os_plain_bytes = (size_t)std::max(0L, env_long("HETCCL_ONESHOT_PLAIN_KB", os_plain_default_kb)) * 1024;
   set_os_layout(c);
   // mid sizes (r02bv/r02bw, 2+2): one tile per channel either way, and 128 channels of larger tiles beat 296 of
   // small ones from 2 to 32 MiB (0.89-1.03x NCCL vs 0.74-0.91x); 1+1 keeps every channel for its pipelined sizes
@@ -285,7 +293,16 @@ hetcclResult_t run_op(hetcclComm_t c, int op, const void* const* sends, void* co
     CUDA_TRY(c, nvls_allreduce(c->nvls, sends[0], recvs[0], count, dt, c->err, c->timeout_ns, stream));
     return hetcclSuccess;
   }
-  bool oneshot = op == OP_ALLREDUCE && c->os_bytes > 0 && count * (size_t)es <= c->os_bytes;
+  // symmetric recv (every rank's recv at the same offset of a connected hetccl_mem_* buffer, the direct-mode
+  // contract below) takes the one-shot up to os_bytes, a plain recv up to os_plain_bytes
+  bool sym_recv = c->kind == KIND_MUX;
+  if (op == OP_ALLREDUCE && !sym_recv && c->direct) {
+    const char* y = (const char*)recvs[0];
+    for (auto& b : c->sym)
+      if (b.connected && y >= b.base && y + count * (size_t)es <= b.base + b.bytes) sym_recv = true;
+  }
+  const size_t os_cut = sym_recv ? c->os_bytes : c->os_plain_bytes;
+  bool oneshot = op == OP_ALLREDUCE && os_cut > 0 && count * (size_t)es <= os_cut;
   OpArgs a;
   memset(&a, 0, sizeof(a));
   a.topo = c->topo;
@@ -551,6 +568,7 @@ hetcclResult_t hetccl_comm_export(hetcclComm_t c, void* blob, size_t* blob_bytes
   b.ws = c->ws;
   b.nslots = c->nslots;
   b.os_bytes = c->os_bytes;
+  b.os_plain_bytes = c->os_plain_bytes;
   b.mid_nch = c->mid_nch;
   b.mid_bytes = c->mid_bytes;
   b.nvls = c->nvls_blob;
@@ -577,7 +595,7 @@ hetcclResult_t hetccl_comm_connect(hetcclComm_t c, const void* blobs, size_t blo
     if (memcmp(b.map, c->map, sizeof(int) * c->n) != 0)
       return fail(c, hetcclInvalidUsage, "rank %d passed a different rank_to_domain map", r);
     if (b.slot_bytes != c->slot_bytes || b.nch_max != c->nch_max || b.ws != c->ws || b.nslots != c->nslots ||
-        b.os_bytes != c->os_bytes || b.mid_nch != c->mid_nch || b.mid_bytes != c->mid_bytes)
+        b.os_bytes != c->os_bytes || b.os_plain_bytes != c->os_plain_bytes || b.mid_nch != c->mid_nch || b.mid_bytes != c->mid_bytes)
       return fail(c, hetcclInvalidUsage, "rank %d has different HETCCL_SLOT_KB/NCHANNELS/WS/NSLOTS/ONESHOT_KB/MID_*", r);
     if (r == c->rank) continue;
     void* p = nullptr;
